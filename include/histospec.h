@@ -1,0 +1,158 @@
+/*
+ * histospec.h -- C-ABI of the B200 HistoSpec hot path (libhistospec.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Device pointers are marked
+ * d_*, host pointers h_*.  Every function returns HS_OK (0) or a negative
+ * HS_ERR_* code; hs_last_error() returns a static message for the last error
+ * on the calling thread.  All kernels are stream-ordered and non-blocking
+ * unless stated otherwise.  The library allocates no persistent device memory:
+ * callers own every buffer (plan -> allocate -> build).
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/rhymesim/):
+ *   hs_index_plan / hs_index_build / hs_index_build_table
+ *       -> history.py:343-355 build_tree, :148-279 SuffixTree.add_response /
+ *          finalize, :417-422 HistoryStore._build_and_swap
+ *   hs_lookup_batch
+ *       -> history.py:283-300 match_prefix, :302-333 extract_draft
+ *   hs_draft
+ *       -> spec_engine.py:206-215 (prefix slice + extract_draft inside
+ *          step_response), batched over sequences
+ *   hs_accept_replay / hs_accept_greedy
+ *       -> spec_engine.py:100-107 verify, :49-53 next_window, :69-72
+ *          choose_prefix, :124-133 SpecStats.record, :217-240 step_response
+ *          (replay: truth supplied; greedy: truth = argmax of the verify rows)
+ *   hs_replay_fused
+ *       -> spec_engine.py:260-279 replay_response, whole responses per launch
+ */
+#ifndef HISTOSPEC_H_
+#define HISTOSPEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_OK 0
+#define HS_ERR_INVALID (-1)   /* maps to ValueError */
+#define HS_ERR_CUDA (-2)      /* CUDA runtime failure */
+#define HS_ERR_SPACE (-3)     /* caller buffer too small */
+
+/* Fixed-point reward scale: reward_fx = reward * 2^HS_REWARD_FRAC_BITS. */
+#define HS_REWARD_FRAC_BITS 32
+/* Extra -1 entries after the text so warp-wide reads never leave the buffer. */
+#define HS_TEXT_PAD 64
+#define HS_MAX_WINDOW 32      /* hs_draft / hs_accept_* window_max limit */
+#define HS_MAX_TABLE_PREFIX 32
+
+typedef void* hs_stream_t;    /* cudaStream_t */
+
+typedef struct {
+  int32_t pos;    /* text position of the heavy occurrence; -1 = empty slot */
+  int32_t tag;    /* hash bits | m */
+  int64_t mass;   /* fixed-point reward mass below the pattern */
+} HsGramEntry;
+
+typedef struct {
+  size_t index_bytes;      /* persistent arrays (text, SA, LCP, mass sums, heavy) */
+  size_t workspace_bytes;  /* scratch, must stay untouched until build_table */
+} HsIndexPlan;
+
+typedef struct {
+  /* persistent device arrays inside the caller's index buffer */
+  const int32_t* text;          /* [n_text + HS_TEXT_PAD]; -1 after each response */
+  const int32_t* sa;            /* [n_suffix] suffix array, slot-major */
+  const int32_t* lcp;           /* [n_suffix + 1]; -1 at slot starts and the end */
+  const int64_t* wsum;          /* [n_suffix + 1] exclusive prefix sums of weights */
+  const int32_t* heavy;         /* [n_suffix] heavy text position per node id */
+  const uint8_t* node_flags;    /* [n_suffix] bit0 node, bit1 has token child */
+  const int64_t* slot_text_off; /* [n_slots + 1] */
+  const int64_t* slot_sa_off;   /* [n_slots + 1] */
+  int64_t* slot_stats;          /* [n_slots, 2]: reference node count, root mass */
+  const HsGramEntry* table;     /* NULL until hs_index_build_table */
+  int64_t table_mask;
+  int64_t n_text, n_suffix;
+  int32_t n_slots, prefix_min, prefix_max, max_len;
+  int32_t n_levels;             /* sparse-table levels kept in the workspace */
+  int64_t n_gram_groups;        /* host copy, valid after hs_index_build returns */
+  void* ws;                     /* workspace pointer used by the build */
+  size_t ws_bytes;
+} HsIndexView;
+
+typedef struct {
+  int32_t enabled, window_init, window_add, window_max, prefix_init, prefix_min;
+} HsSpecConfig;
+
+const char* hs_last_error(void);
+int hs_version(void);
+
+/* Sizes for a build over n_tokens tokens in n_resp responses / n_slots slots. */
+int hs_index_plan(int64_t n_tokens, int32_t n_resp, int32_t n_slots, int32_t max_len,
+                  int32_t prefix_min, int32_t prefix_max, HsIndexPlan* plan);
+
+/* K1a: suffix array, LCP, LCP-interval tree, heavy continuations.
+ * Responses must be grouped by slot: slot s owns responses
+ * [h_slot_resp_off[s], h_slot_resp_off[s+1]).  Synchronizes `stream` once
+ * at the end (to read the n-gram group count). */
+int hs_index_build(const int32_t* d_tokens, int64_t n_tokens,
+                   const int64_t* h_resp_off, int32_t n_resp,
+                   const int64_t* h_slot_resp_off, int32_t n_slots,
+                   const int64_t* h_reward_fx, int32_t prefix_min, int32_t prefix_max,
+                   void* d_index, size_t index_bytes, void* d_ws, size_t ws_bytes,
+                   HsIndexView* view, hs_stream_t stream);
+
+/* K1b: n-gram -> heavy-occurrence hash table for m in [prefix_min, prefix_max]. */
+int hs_index_table_bytes(const HsIndexView* view, size_t* bytes);
+int hs_index_build_table(HsIndexView* view, void* d_table, size_t table_bytes, hs_stream_t stream);
+
+/* General lookups (any prefix length / window): binary search over the SA.
+ * out_info[i*6 + {0..5}] = found, draft_len, mass_fx, at_node, heavy_pos, locus_depth. */
+int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t* d_slot,
+                    const int32_t* d_prefix, int32_t prefix_stride, const int32_t* d_prefix_len,
+                    const int32_t* d_window, int32_t* d_out_tok, int32_t out_stride,
+                    int64_t* d_out_info, int32_t use_table, hs_stream_t stream);
+
+/* K2: batched draft proposal for the rollout step (warp per sequence).
+ * Looks up iff speculate[s] && gen_len[s] >= prefix_len[s] (spec_engine.py:210),
+ * using the last prefix_len generated tokens of row s. */
+int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq,
+             const int32_t* d_gen_tok, int32_t gen_stride, const int32_t* d_gen_len,
+             const int32_t* d_prefix_len, const int32_t* d_window, const uint8_t* d_speculate,
+             int32_t* d_draft_tok, int32_t draft_stride, int32_t* d_draft_len,
+             uint8_t* d_looked, uint8_t* d_found, hs_stream_t stream);
+
+/* K6 (replay): accept against supplied truth rows; appends accepted + bonus to
+ * gen rows, updates window / prefix / stats[n,5] and optionally records
+ * tokens-per-iteration (d_tpi may be NULL). */
+int hs_accept_replay(int32_t n_seq, const int32_t* d_truth, int32_t truth_stride,
+                     const int32_t* d_target_len, const int32_t* d_draft_tok, int32_t draft_stride,
+                     const int32_t* d_draft_len, const uint8_t* d_looked, const uint8_t* d_found,
+                     int32_t* d_gen_tok, int32_t gen_stride, int32_t* d_gen_len,
+                     int32_t* d_window, int32_t* d_prefix_len, int64_t* d_stats,
+                     int32_t* d_tpi, int32_t tpi_stride, int32_t* d_n_iter,
+                     HsSpecConfig cfg, hs_stream_t stream);
+
+/* K6 (greedy): truth = argmax rows of the verify forward.  Row q_off[s] + i
+ * holds the model's next-token argmax after consuming [last, d_1..d_i].
+ * Also rolls back kv_len[s] to prompt_len + gen_len_new - 1 (the bonus
+ * token's KV is written by the next forward). */
+int hs_accept_greedy(int32_t n_seq, const int32_t* d_argmax, const int32_t* d_q_off,
+                     const int32_t* d_target_len, const int32_t* d_draft_tok, int32_t draft_stride,
+                     const int32_t* d_draft_len, const uint8_t* d_looked, const uint8_t* d_found,
+                     int32_t* d_gen_tok, int32_t gen_stride, int32_t* d_gen_len,
+                     int32_t* d_window, int32_t* d_prefix_len, int64_t* d_stats,
+                     int32_t* d_tpi, int32_t tpi_stride, int32_t* d_n_iter,
+                     HsSpecConfig cfg, hs_stream_t stream);
+
+/* Whole-response replay in one launch (warp per response): K2 + K6 fused. */
+int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq,
+                    const int32_t* d_truth, const int64_t* d_truth_off, const uint8_t* d_speculate,
+                    int32_t* d_tpi, int32_t* d_n_iter, int64_t* d_stats, HsSpecConfig cfg,
+                    hs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HISTOSPEC_H_ */

@@ -1,0 +1,43 @@
+// Shared device helpers for the HistoSpec kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "../../include/histospec.h"
+
+#define HS_CUDA_TRY(expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) { hs_set_error(cudaGetErrorString(_e)); return HS_ERR_CUDA; } \
+  } while (0)
+
+void hs_set_error(const char* msg);
+
+namespace hs {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+// 64-bit hash of (slot, m, tokens[0..m)).  Same function is used at build and
+// probe time; collisions are harmless because every hit is verified against
+// the text.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27; x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+__host__ __device__ __forceinline__ uint64_t gram_hash(int32_t slot, int32_t m, const int32_t* tok) {
+  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
+  for (int j = 0; j < m; ++j) h = mix64(h ^ ((uint64_t)(uint32_t)tok[j] * 0x9E3779B97F4A7C15ULL));
+  return h;
+}
+
+// Hash-table tag: high bits of the hash with m in the low 6 bits.
+__host__ __device__ __forceinline__ int32_t gram_tag(uint64_t h, int32_t m) {
+  return (int32_t)(((uint32_t)(h >> 32) & ~0x3Fu) | (uint32_t)m);
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+}  // namespace hs

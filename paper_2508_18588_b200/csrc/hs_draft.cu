@@ -1,0 +1,261 @@
+// K2: batched draft proposal (warp per sequence) + general SA lookups.
+//
+// Hot path (spec_engine.py:206-215 -> history.py:302-333): the last m
+// generated tokens are hashed, 32 consecutive table entries are probed with
+// one coalesced 512 B warp load, a tag hit is verified against the text by
+// m lanes at once (ballot), and the draft is text[heavy + m : ...] read by
+// `window` lanes in one coalesced load, cut at the first terminal (ballot).
+//
+// General path (any prefix length, history.py:283-300 match_prefix): warp
+// binary search over the slot's suffix array with warp-parallel comparisons,
+// then the locus node from a warp min-scan of the LCP values inside the
+// interval.
+#include "hs_common.cuh"
+
+namespace hs {
+
+struct Hit {
+  int32_t found;
+  int32_t pos;      // heavy text position (draft = text[pos + m ...])
+  int64_t mass;
+  int32_t at_node;
+  int32_t depth;    // depth of the locus (m for a match that ends on a node)
+};
+
+// Each lane j < m holds pre_j = prefix token j (lanes >= m: ignored).
+__device__ __forceinline__ Hit probe_table(const HsIndexView& V, int32_t slot, int32_t m, int32_t pre_j) {
+  const int lane = lane_id();
+  // every lane computes the same hash from broadcast tokens
+  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
+  for (int j = 0; j < m; ++j) {
+    int32_t t = __shfl_sync(0xffffffffu, pre_j, j);
+    h = mix64(h ^ ((uint64_t)(uint32_t)t * 0x9E3779B97F4A7C15ULL));
+  }
+  const int32_t tag = gram_tag(h, m);
+  const int64_t lo = V.slot_text_off[slot], hi = V.slot_text_off[slot + 1];
+  int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
+  Hit r{0, -1, 0, 0, 0};
+  for (;;) {
+    HsGramEntry e = V.table[(base + lane) & V.table_mask];
+    bool empty = e.pos < 0;
+    bool cand = !empty && e.tag == tag && e.pos >= lo && e.pos < hi;
+    unsigned empties = __ballot_sync(0xffffffffu, empty);
+    unsigned cands = __ballot_sync(0xffffffffu, cand);
+    // lanes before the first empty slot are the live probe sequence
+    unsigned live = empties ? ((1u << (__ffs(empties) - 1)) - 1u) : 0xffffffffu;
+    cands &= live;
+    while (cands) {
+      int src = __ffs(cands) - 1;
+      int32_t pos = __shfl_sync(0xffffffffu, e.pos, src);
+      int32_t t = lane < m ? V.text[pos + lane] : 0;
+      unsigned bad = __ballot_sync(0xffffffffu, lane < m && t != pre_j);
+      if (!bad) {
+        r.found = 1;
+        r.pos = pos;
+        r.mass = __shfl_sync(0xffffffffu, e.mass, src);
+        return r;
+      }
+      cands &= cands - 1;
+    }
+    if (empties) return r;
+    base += 32;
+  }
+}
+
+// Three-way compare of the first m tokens of suffix p with the prefix
+// (held in lanes, chunked by 32). Returns <0, 0, >0 (suffix vs prefix).
+__device__ __forceinline__ int cmp_suffix(const int32_t* __restrict__ text, int32_t p,
+                                          const int32_t* __restrict__ pre, int32_t m) {
+  const int lane = lane_id();
+  for (int32_t c = 0; c < m; c += 32) {
+    int32_t j = c + lane;
+    int32_t a = 0, b = 0;
+    bool diff = false;
+    if (j < m) {
+      a = text[p + j];
+      b = pre[j];
+      diff = a != b;
+    }
+    unsigned d = __ballot_sync(0xffffffffu, diff);
+    if (d) {
+      int src = __ffs(d) - 1;
+      int32_t x = __shfl_sync(0xffffffffu, a, src);
+      int32_t y = __shfl_sync(0xffffffffu, b, src);
+      return x < y ? -1 : 1;   // the terminal (-1) sorts below every token
+    }
+  }
+  return 0;
+}
+
+__device__ Hit lookup_general(const HsIndexView& V, int32_t slot, const int32_t* __restrict__ pre, int32_t m) {
+  const int lane = lane_id();
+  Hit r{0, -1, 0, 0, 0};
+  int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
+  // lower bound: first suffix whose m-prefix >= pre
+  int64_t lo = S, hi = E;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cmp_suffix(V.text, V.sa[mid], pre, m) < 0) lo = mid + 1; else hi = mid;
+  }
+  int64_t first = lo;
+  hi = E;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cmp_suffix(V.text, V.sa[mid], pre, m) <= 0) lo = mid + 1; else hi = mid;
+  }
+  int64_t last = lo;  // exclusive
+  if (first == last) return r;
+  r.found = 1;
+  r.mass = V.wsum[last] - V.wsum[first];
+  if (last - first == 1) {
+    r.pos = V.sa[first];
+    r.depth = m;   // inside a leaf edge (the terminal follows at the earliest)
+    r.at_node = 0;
+    return r;
+  }
+  // locus: first position of the minimum LCP inside (first, last)
+  int32_t best = 0x7fffffff;
+  int64_t bidx = -1;
+  for (int64_t k = first + 1 + lane; k < last; k += 32) {
+    int32_t v = V.lcp[k];
+    if (v < best) { best = v; bidx = k; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    int32_t ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ov < best || (ov == best && oi >= 0 && (bidx < 0 || oi < bidx))) { best = ov; bidx = oi; }
+  }
+  r.pos = V.heavy[bidx];
+  r.depth = best;
+  r.at_node = (best == m) && (V.node_flags[bidx] & 2) ? 1 : 0;
+  return r;
+}
+
+// Copy up to `window` draft tokens text[pos + m ...] into out, stop at the terminal.
+__device__ __forceinline__ int32_t read_draft(const int32_t* __restrict__ text, int32_t start, int32_t window,
+                                              int32_t* __restrict__ out) {
+  const int lane = lane_id();
+  int32_t len = 0;
+  for (int32_t c = 0; c < window; c += 32) {
+    int32_t j = c + lane;
+    int32_t t = j < window ? text[start + j] : 0;
+    unsigned term = __ballot_sync(0xffffffffu, j < window && t < 0);
+    int32_t lim = term ? (__ffs(term) - 1) : 32;
+    if (lane < lim && j < window) out[j] = t;
+    if (term) return len + lim;
+    len += (window - c) < 32 ? (window - c) : 32;
+  }
+  return len;
+}
+
+__global__ void k_lookup_batch(HsIndexView V, int32_t n, const int32_t* __restrict__ slot,
+                               const int32_t* __restrict__ prefix, int32_t prefix_stride,
+                               const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ window,
+                               int32_t* __restrict__ out_tok, int32_t out_stride, int64_t* __restrict__ info,
+                               int32_t use_table) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const int lane = lane_id();
+  int32_t s = slot[w], m = prefix_len[w], win = window[w];
+  const int32_t* pre = prefix + (int64_t)w * prefix_stride;
+  Hit h;
+  if (s < 0 || s >= V.n_slots || m < 1) {
+    h = Hit{0, -1, 0, 0, 0};
+  } else if (use_table && V.table && m >= V.prefix_min && m <= V.prefix_max) {
+    int32_t pj = lane < m ? pre[lane] : 0;
+    h = probe_table(V, s, m, pj);
+  } else {
+    h = lookup_general(V, s, pre, m);
+  }
+  int32_t len = 0;
+  if (h.found && win > 0) len = read_draft(V.text, h.pos + m, win, out_tok + (int64_t)w * out_stride);
+  if (lane == 0) {
+    int64_t* o = info + 6 * w;
+    o[0] = h.found;
+    o[1] = len;
+    o[2] = h.mass;
+    o[3] = h.at_node;
+    o[4] = h.pos;
+    o[5] = h.depth;
+  }
+}
+
+// K2 hot path: one warp per sequence.
+__global__ void __launch_bounds__(256) k_draft(HsIndexView V, int32_t n_seq, const int32_t* __restrict__ slot_of_seq,
+                                               const int32_t* __restrict__ gen_tok, int32_t gen_stride,
+                                               const int32_t* __restrict__ gen_len,
+                                               const int32_t* __restrict__ prefix_len,
+                                               const int32_t* __restrict__ window,
+                                               const uint8_t* __restrict__ speculate,
+                                               int32_t* __restrict__ draft_tok, int32_t draft_stride,
+                                               int32_t* __restrict__ draft_len, uint8_t* __restrict__ looked,
+                                               uint8_t* __restrict__ found) {
+  int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_seq) return;
+  const int lane = lane_id();
+  int32_t m = prefix_len[s], pos = gen_len[s], slot = slot_of_seq[s];
+  bool look = speculate[s] && slot >= 0 && pos >= m;
+  int32_t len = 0;
+  bool hit = false;
+  if (look) {
+    const int32_t* row = gen_tok + (int64_t)s * gen_stride + pos - m;
+    Hit h;
+    if (V.table && m >= V.prefix_min && m <= V.prefix_max) {
+      int32_t pj = lane < m ? row[lane] : 0;
+      h = probe_table(V, slot, m, pj);
+    } else {
+      h = lookup_general(V, slot, row, m);
+    }
+    hit = h.found;
+    if (hit) len = read_draft(V.text, h.pos + m, window[s], draft_tok + (int64_t)s * draft_stride);
+  }
+  if (lane == 0) {
+    draft_len[s] = len;
+    looked[s] = look;
+    found[s] = hit;
+  }
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+extern "C" int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t* d_slot, const int32_t* d_prefix,
+                               int32_t prefix_stride, const int32_t* d_prefix_len, const int32_t* d_window,
+                               int32_t* d_out_tok, int32_t out_stride, int64_t* d_out_info, int32_t use_table,
+                               hs_stream_t stream) {
+  if (n <= 0) return HS_OK;
+  if (view->n_suffix == 0) {
+    HS_CUDA_TRY(cudaMemsetAsync(d_out_info, 0, sizeof(int64_t) * 6 * n, (cudaStream_t)stream));
+    return HS_OK;
+  }
+  int threads = 256;
+  int64_t blocks = ((int64_t)n * 32 + threads - 1) / threads;
+  k_lookup_batch<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n, d_slot, d_prefix, prefix_stride,
+                                                                       d_prefix_len, d_window, d_out_tok, out_stride,
+                                                                       d_out_info, use_table);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
+extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq, const int32_t* d_gen_tok,
+                        int32_t gen_stride, const int32_t* d_gen_len, const int32_t* d_prefix_len,
+                        const int32_t* d_window, const uint8_t* d_speculate, int32_t* d_draft_tok,
+                        int32_t draft_stride, int32_t* d_draft_len, uint8_t* d_looked, uint8_t* d_found,
+                        hs_stream_t stream) {
+  if (n_seq <= 0) return HS_OK;
+  if (draft_stride < 1) { hs_set_error("draft_stride"); return HS_ERR_INVALID; }
+  int threads = 256;
+  int64_t blocks = ((int64_t)n_seq * 32 + threads - 1) / threads;
+  HsIndexView V = *view;
+  if (V.n_suffix == 0) {
+    // empty history: every lookup misses
+    V.table = nullptr;
+  }
+  k_draft<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
+                                                                 d_gen_len, d_prefix_len, d_window, d_speculate,
+                                                                 d_draft_tok, draft_stride, d_draft_len, d_looked,
+                                                                 d_found);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
