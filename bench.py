@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""HistoSpec B200 benchmark (driver contract: one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload rollout|replay|lookup]
+
+Workloads (all on BASELINE.json configs[1] shapes, synthetic, seeded):
+  rollout  greedy HistoSpec rollout of the Qwen2.5-1.5B-shaped random-init
+           policy (512 prompts x 8 samples x 4k tokens); see engine.py
+  replay   the reference's own path without a model: GPU history ingest (K1)
+           + draft/verify/accept replay (K2+K6) of 4096 x 4096-token rollouts
+  lookup   K2 draft-lookup microbenchmark over every position of an epoch
+
+--impl reference times the reference algorithm on the host cores (the C
+oracle port in oracle/, all threads) on a bounded sample of the same workload.
+Under torchrun (N > 1) every rank runs its own shard (weak scaling); timing is
+CUDA events on the launching stream, max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+# ------------------------------------------------------------------ helpers
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "bf16_tflops": float(p["bf16_tflops"]),
+                "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "measured"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if not self.path or not os.path.exists(self.path):
+            return out
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(smax), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+class Dist:
+    def __init__(self, backend):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if backend == "nccl":
+                import torch
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg is not None:
+            if self.pg.get_backend() == "nccl":
+                import torch
+                self.pg.barrier(device_ids=[self.local])
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.pg is None:
+            return x
+        import torch
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+def timed(fn, steps, warmup, dist, stream, gpu_index):
+    """W untimed + exactly K timed calls bracketed by barrier + synchronize; returns (ms/step, clocks)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_index) as clk:
+        start.record(stream)
+        for _ in range(steps):
+            fn()
+        end.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / steps
+    return dist.max(ms), clk.summary()
+
+
+# ------------------------------------------------------------------ replay workload
+
+def replay_setup(args, rank):
+    import torch
+    from paper_2508_18588_b200.workload import ReplayWorkload
+    wl = ReplayWorkload(prompts=args.prompts, samples=args.samples, length=args.length,
+                        similarity=args.similarity, shard=rank, seed=args.seed)
+    data = wl.generate()
+    return wl, data
+
+
+def cpu_replay_sample(data, sample_prompts, threads):
+    """Reference algorithm on the host (oracle C port): ingest + replay a bounded sample."""
+    from oracle import hs_oracle_c as C
+    P = min(sample_prompts, len(data["slot_resp_off"]) - 1)
+    so, ro = data["slot_resp_off"], data["resp_off"]
+    n_resp = int(so[P])
+    L = int(ro[1] - ro[0])
+    toks = data["hist_tokens"][:int(ro[n_resp])].reshape(n_resp, L)
+    text = np.concatenate([toks, np.full((n_resp, 1), -1, np.int32)], axis=1).reshape(-1).astype(np.int32)
+    rid = np.repeat(np.arange(n_resp, dtype=np.int32), L + 1)
+    rew = data["rewards"][:n_resp].astype(np.float64)
+    poff = (np.asarray(so[:P + 1]) * (L + 1)).astype(np.int64)
+    samples = len(data["truth_slots"]) // (len(so) - 1)
+    n_truth = P * samples
+    truths = data["truths"][:n_truth]
+    tcat = truths.reshape(-1).astype(np.int32)
+    toff = (np.arange(n_truth + 1, dtype=np.int64) * truths.shape[1])
+    tslot = data["truth_slots"][:n_truth].astype(np.int32)
+    has = np.ones(P, np.uint8)
+    t0 = time.perf_counter()
+    tpi, niter, stats = C.replay_arrays(text, rid, rew, poff, has, tcat, toff, tslot, (1, 2, 2, 32, 7, 3), 1,
+                                        threads)
+    dt = time.perf_counter() - t0
+    tok = int(stats[:, 0].sum())
+    return {"tokens": tok, "seconds": dt, "value": tok / dt, "stats": stats.sum(axis=0).tolist(),
+            "sample": f"{P} prompts x {samples} samples x {truths.shape[1]} tokens (ingest + replay)"}
+
+
+def run_replay(args, dist, pk):
+    import torch
+    from paper_2508_18588_b200 import _lib
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.spec_engine import ReplayBuffers, SpecConfig
+
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    wl, data = replay_setup(args, dist.rank)
+    cfg = SpecConfig()
+    stream = torch.cuda.current_stream(dev)
+    n_truth = data["truths"].shape[0]
+    L = data["truths"].shape[1]
+    toff = np.arange(n_truth + 1, dtype=np.int64) * L
+    d_hist = torch.from_numpy(data["hist_tokens"]).to(dev)
+    bufs = ReplayBuffers.from_host(data["truths"].reshape(-1), toff, data["truth_slots"],
+                                   np.ones(n_truth, np.uint8), dev)
+    phase = {"build": [], "replay": []}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    state = {}
+
+    def step():
+        ev[0].record(stream)
+        idx = GpuIndex.from_arrays(d_hist, data["resp_off"], data["slot_resp_off"], data["reward_fx"])
+        ev[1].record(stream)
+        bufs.run(idx, cfg, stream)
+        ev[2].record(stream)
+        state["idx"] = idx
+        state["pending"] = True
+
+    def step_and_log():
+        step()
+        torch.cuda.synchronize()
+        phase["build"].append(ev[0].elapsed_time(ev[1]))
+        phase["replay"].append(ev[1].elapsed_time(ev[2]))
+
+    # phase breakdown (untimed pass) then the contract timing
+    step_and_log()
+    lc0 = _lib.load().hs_launch_count()
+    ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
+    launches = (_lib.load().hs_launch_count() - lc0) // (args.steps + args.warmup)
+    step_and_log()
+    st = bufs.stats.cpu().numpy().sum(axis=0)
+    tokens = int(st[0])
+    total_tokens = dist.sum(tokens)
+    value = total_tokens / (ms / 1e3)
+
+    # e2e: public API with host buffers (H2D of history + truths, D2H of results inside the region)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    h_hist = pin(data["hist_tokens"])
+    h_truth = pin(data["truths"].reshape(-1))
+    h_slots = pin(data["truth_slots"])
+    h_toff = pin(toff)
+    h_spec = pin(np.ones(n_truth, np.uint8))
+    out_tpi = torch.empty(int(toff[-1]), dtype=torch.int32).pin_memory()
+    out_stats = torch.empty((n_truth, 5), dtype=torch.int64).pin_memory()
+
+    def e2e_step():
+        d_h = h_hist.to(dev, non_blocking=True)
+        idx = GpuIndex.from_arrays(d_h, data["resp_off"], data["slot_resp_off"], data["reward_fx"])
+        b = ReplayBuffers(truth=h_truth.to(dev, non_blocking=True), truth_off=h_toff.to(dev, non_blocking=True),
+                          slots=h_slots.to(dev, non_blocking=True), speculate=h_spec.to(dev, non_blocking=True),
+                          tpi=torch.empty(int(toff[-1]), dtype=torch.int32, device=dev),
+                          n_iter=torch.empty(n_truth, dtype=torch.int32, device=dev),
+                          stats=torch.empty((n_truth, 5), dtype=torch.int64, device=dev))
+        b.run(idx, cfg, stream)
+        out_tpi.copy_(b.tpi, non_blocking=True)
+        out_stats.copy_(b.stats, non_blocking=True)
+
+    e2e_ms, _ = timed(e2e_step, args.steps, max(1, args.warmup // 2), dist, stream, dist.local)
+    h2d = h_hist.numel() * 4 + h_truth.numel() * 4 + h_slots.numel() * 4 + h_toff.numel() * 8 + n_truth
+    d2h = out_tpi.numel() * 4 + out_stats.numel() * 8
+
+    # roofline: the fused replay kernel (K2+K6, one launch per step)
+    rep_ms = float(np.median(phase["replay"]))
+    build_ms = float(np.median(phase["build"]))
+    iters_lookup = int(st[3] + st[4])
+    # per iteration: prefix (4*7) + probe entry 16 + verify text 4*7 + truth compare/draft 8*k + tpi 4
+    alg_bytes = iters_lookup * (28 + 16 + 28 + 4) + int(st[1]) * 8 + n_truth * (5 * 8 + 4 + 4 + 8 + 4)
+    achieved = alg_bytes / (rep_ms / 1e3) / 1e9
+    line = {
+        "metric": "rollout tokens/sec (HistoSpec replay path: ingest + draft + verify/accept, truth supplied)",
+        "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (D)-history s=%.2f, seeded" % args.similarity,
+        "config": {"workload": "configs[1] shape, replay: %d prompts x %d samples x %d tokens per GPU, G=%d history"
+                               % (args.prompts, args.samples, args.length, 8),
+                   "l2": "inputs (%.0f MB) + index build traffic exceed the 126 MB L2" % (
+                       (d_hist.numel() + bufs.truth.numel()) * 4 / 1e6)},
+        "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
+        "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
+        "acceptance_rate": float(st[2] / max(st[1], 1)),
+        "phases_ms": {"ingest_k1": build_ms, "replay_k2_k6": rep_ms},
+        "e2e": {"value": dist.sum(tokens) / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "k_replay_fused", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "peak_source": pk["source"]},
+        "clocks": clocks,
+    }
+    return line, data
+
+
+# ------------------------------------------------------------------ lookup microbenchmark
+
+def run_lookup(args, dist, pk):
+    import ctypes
+    import torch
+    from paper_2508_18588_b200 import _lib
+    from paper_2508_18588_b200.index import GpuIndex
+
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    wl, data = replay_setup(args, dist.rank)
+    idx = GpuIndex.from_arrays(torch.from_numpy(data["hist_tokens"]).to(dev), data["resp_off"],
+                               data["slot_resp_off"], data["reward_fx"])
+    # one query per truth position (sliding 7-gram windows via gen_stride = 1)
+    P, L = args.prompts, args.length
+    truths = data["truths"][::args.samples]           # one row per prompt
+    flat = torch.from_numpy(truths.reshape(-1).astype(np.int32)).to(dev)
+    m = 7
+    # query s = prefix flat[s : s+m] (gen_stride = 1 turns one buffer into n overlapping rows);
+    # the m-1 windows per prompt that straddle a prompt boundary are ordinary misses/hits of slot s // L
+    n = P * L - m
+    slot = (torch.arange(n, device=dev) // L).to(torch.int32)
+    gen_len = torch.full((n,), m, dtype=torch.int32, device=dev)
+    prefix_len = torch.full((n,), m, dtype=torch.int32, device=dev)
+    window = torch.full((n,), 32, dtype=torch.int32, device=dev)
+    spec = torch.ones(n, dtype=torch.uint8, device=dev)
+    out = torch.empty((n, 32), dtype=torch.int32, device=dev)
+    dlen = torch.empty(n, dtype=torch.int32, device=dev)
+    looked = torch.empty(n, dtype=torch.uint8, device=dev)
+    found = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lib = _lib.load()
+
+    def launch():
+        _lib.check(lib.hs_draft(ctypes.byref(idx.view), n, slot.data_ptr(), flat.data_ptr(), 1, gen_len.data_ptr(),
+                                prefix_len.data_ptr(), window.data_ptr(), spec.data_ptr(), out.data_ptr(), 32,
+                                dlen.data_ptr(), looked.data_ptr(), found.data_ptr(), stream.cuda_stream))
+
+    ms, clocks = timed(launch, args.steps, args.warmup, dist, stream, dist.local)
+    dl = int(dlen.sum().item())
+    hits = int(found.sum().item())
+    alg = n * (4 + 16 + 4 * m + 4 * 4 + 3) + hits * 0 + dl * 8
+    achieved = alg / (ms / 1e3) / 1e9
+    return {
+        "metric": "draft lookups/sec (K2 hs_draft, every position of an epoch)", "value": dist.sum(n) / (ms / 1e3),
+        "unit": "queries/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{n} queries (m=7, window 32) over {P} prompts x 8 x {L}-token (D) histories",
+                   "l2": "index + outputs exceed L2"},
+        "hit_rate": hits / n, "mean_draft_len": dl / n,
+        "roofline": {"kernel": "k_draft", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "bytes_per_query": alg / n},
+        "gpu_launches": 1, "clocks": clocks,
+    }, data
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    from paper_2508_18588_b200.workload import ReplayWorkload
+    wl = ReplayWorkload(prompts=args.ref_prompts, samples=args.samples, length=args.length,
+                        similarity=args.similarity, shard=0, seed=args.seed)
+    data = wl.generate()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_replay_sample(data, args.ref_prompts, threads)
+        if i >= args.warmup:
+            vals.append(r)
+    tok = sum(r["tokens"] for r in vals)
+    sec = sum(r["seconds"] for r in vals)
+    value = tok / sec
+    st = np.sum([r["stats"] for r in vals], axis=0)
+    return {
+        "impl": "reference", "metric": "rollout tokens/sec (HistoSpec replay path: ingest + draft + verify/accept, "
+                                      "truth supplied)",
+        "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sec / len(vals), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic (D)-history s=%.2f, seeded" % args.similarity,
+        "config": {"workload": "configs[1] shape, replay (reference algorithm on host cores)"},
+        "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="replay", choices=["replay", "lookup"])
+    ap.add_argument("--prompts", type=int, default=512)
+    ap.add_argument("--samples", type=int, default=8)
+    ap.add_argument("--length", type=int, default=4096)
+    ap.add_argument("--similarity", type=float, default=0.7)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ref-prompts", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        dist = Dist("gloo")
+        line = run_reference(args, dist)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        dist.close()
+        return
+
+    dist = Dist("nccl")
+    pk = peaks()
+    if args.workload == "replay":
+        line, data = run_replay(args, dist, pk)
+    else:
+        line, data = run_lookup(args, dist, pk)
+    if dist.rank == 0:
+        if dist.world == 1 and not args.no_cpu_baseline and args.workload == "replay":
+            r = cpu_replay_sample(data, args.ref_prompts, os.cpu_count() or 1)
+            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": r["sample"]}
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

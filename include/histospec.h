@@ -87,6 +87,8 @@ typedef struct {
 
 const char* hs_last_error(void);
 int hs_version(void);
+/* Number of this library's own kernel launches so far (process-wide). */
+int64_t hs_launch_count(void);
 
 /* Sizes for a build over n_tokens tokens in n_resp responses / n_slots slots. */
 int hs_index_plan(int64_t n_tokens, int32_t n_resp, int32_t n_slots, int32_t max_len,

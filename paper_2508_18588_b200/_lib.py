@@ -46,6 +46,7 @@ class HsSpecConfig(ctypes.Structure):
 _P, _I32, _I64, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
 SIGNATURES = {
     "hs_version": [],
+    "hs_launch_count": [],
     "hs_last_error": None,
     "hs_index_plan": [_I64, _I32, _I32, _I32, _I32, _I32, ctypes.POINTER(HsIndexPlan)],
     "hs_index_build": [_P, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P, _SZ, _P, _SZ,
@@ -79,6 +80,9 @@ def load(path: str = LIB_PATH):
                 fn = getattr(lib, name)
                 if name == "hs_last_error":
                     fn.restype = ctypes.c_char_p
+                    fn.argtypes = []
+                elif name == "hs_launch_count":
+                    fn.restype = ctypes.c_int64
                     fn.argtypes = []
                 else:
                     fn.restype = ctypes.c_int

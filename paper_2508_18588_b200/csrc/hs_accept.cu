@@ -309,6 +309,7 @@ extern "C" int hs_accept_replay(int32_t n_seq, const int32_t* d_truth, int32_t t
   if (rc) return rc;
   if (n_seq <= 0) return HS_OK;
   int64_t blocks = ((int64_t)n_seq * 32 + 255) / 256;
+  hs_count_launches(1);
   acc::k_accept_replay<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       n_seq, d_truth, truth_stride, d_target_len, d_draft_tok, draft_stride, d_draft_len, d_looked, d_found, d_gen_tok,
       gen_stride, d_gen_len, d_window, d_prefix_len, d_stats, d_tpi, tpi_stride, d_n_iter, cfg);
@@ -326,6 +327,7 @@ extern "C" int hs_accept_greedy(int32_t n_seq, const int32_t* d_argmax, const in
   if (rc) return rc;
   if (n_seq <= 0) return HS_OK;
   int64_t blocks = ((int64_t)n_seq * 32 + 255) / 256;
+  hs_count_launches(1);
   acc::k_accept_greedy<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       n_seq, d_argmax, d_q_off, d_target_len, d_draft_tok, draft_stride, d_draft_len, d_looked, d_found, d_gen_tok,
       gen_stride, d_gen_len, d_window, d_prefix_len, d_stats, d_tpi, tpi_stride, d_n_iter, cfg);
@@ -342,6 +344,7 @@ extern "C" int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int
   if (n_seq <= 0) return HS_OK;
   HsIndexView V = *view;
   int64_t blocks = ((int64_t)n_seq * 32 + 255) / 256;
+  hs_count_launches(1);
   acc::k_replay_fused<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_truth,
                                                                         d_truth_off, d_speculate, d_tpi, d_n_iter,
                                                                         d_stats, cfg);

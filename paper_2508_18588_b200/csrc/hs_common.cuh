@@ -11,6 +11,7 @@
   } while (0)
 
 void hs_set_error(const char* msg);
+void hs_count_launches(int64_t n);
 
 namespace hs {
 

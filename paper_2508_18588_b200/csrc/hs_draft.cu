@@ -231,6 +231,7 @@ extern "C" int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t
   }
   int threads = 256;
   int64_t blocks = ((int64_t)n * 32 + threads - 1) / threads;
+  hs_count_launches(1);
   k_lookup_batch<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n, d_slot, d_prefix, prefix_stride,
                                                                        d_prefix_len, d_window, d_out_tok, out_stride,
                                                                        d_out_info, use_table);
@@ -252,6 +253,7 @@ extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d
     // empty history: every lookup misses
     V.table = nullptr;
   }
+  hs_count_launches(1);
   k_draft<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
                                                                  d_gen_len, d_prefix_len, d_window, d_speculate,
                                                                  d_draft_tok, draft_stride, d_draft_len, d_looked,

@@ -480,6 +480,10 @@ thread_local char g_err[512];
 
 void hs_set_error(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
 
+static int64_t g_launches = 0;
+void hs_count_launches(int64_t n) { __atomic_fetch_add(&g_launches, n, __ATOMIC_RELAXED); }
+extern "C" int64_t hs_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 extern "C" const char* hs_last_error(void) { return g_err; }
 extern "C" int hs_version(void) { return 1; }
 
@@ -604,6 +608,7 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
     return HS_OK;
   }
 
+  hs_count_launches(1);
   k_layout<<<n_resp, 256, 0, st>>>(d_tokens, L.resp_off, L.resp_slot, n_resp, L.text, L.rid, L.rem,
                                    L.sufpos, L.keys);
   HS_CUDA_TRY(cudaGetLastError());
@@ -616,8 +621,10 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
     cub::DoubleBuffer<uint64_t> dk(L.keys, L.keys_alt);
     cub::DoubleBuffer<int32_t> dv(L.sufpos, L.sa_alt);
     HS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cub_bytes, dk, dv, (int)n, 0, 32 + slot_bits, st));
+    hs_count_launches(1);
     k_group_head<<<blocks(n), 256, 0, st>>>(dk.Current(), n, L.head);
     HS_CUDA_TRY(cub::DeviceScan::InclusiveScan(L.cub_tmp, cub_bytes, L.head, L.gstart, cub::Max(), (int)n, st));
+    hs_count_launches(1);
     k_scatter_rank<<<blocks(n), 256, 0, st>>>(dv.Current(), L.gstart, n, rank_ptrs[0]);
     HS_CUDA_TRY(cudaMemcpyAsync(L.sa, dv.Current(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
   }
@@ -625,30 +632,38 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
   for (int j = 0; j < d.rounds; ++j) {
     int32_t h = 1 << j;
     // keys from the previous order (any order works; reuse sa to keep locality)
+    hs_count_launches(1);
     k_double_keys<<<blocks(n), 256, 0, st>>>(L.sa, rank_ptrs[j], L.rem, n, h, rank_bits, L.keys);
     HS_CUDA_TRY(cudaMemcpyAsync(L.sufpos, L.sa, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
     cub::DoubleBuffer<uint64_t> dk(L.keys, L.keys_alt);
     cub::DoubleBuffer<int32_t> dv(L.sufpos, L.sa_alt);
     HS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cub_bytes, dk, dv, (int)n, 0, 2 * rank_bits, st));
+    hs_count_launches(1);
     k_group_head<<<blocks(n), 256, 0, st>>>(dk.Current(), n, L.head);
     HS_CUDA_TRY(cub::DeviceScan::InclusiveScan(L.cub_tmp, cub_bytes, L.head, L.gstart, cub::Max(), (int)n, st));
+    hs_count_launches(1);
     k_scatter_rank<<<blocks(n), 256, 0, st>>>(dv.Current(), L.gstart, n, rank_ptrs[j + 1]);
     HS_CUDA_TRY(cudaMemcpyAsync(L.sa, dv.Current(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
   }
   HS_CUDA_TRY(cudaGetLastError());
 
   // ---- LCP, weights, sparse table
+  hs_count_launches(1);
   k_lcp<<<blocks(n + 1), 256, 0, st>>>(L.sa, L.rem, L.rid, L.resp_slot, L.rank_ptrs, d.rounds, n, L.lcp);
+  hs_count_launches(1);
   k_weights<<<blocks(n + 1), 256, 0, st>>>(L.sa, L.rid, L.reward, n, L.wtmp);
   HS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cub_bytes, L.wtmp, L.wsum, (int)(n + 1), st));
-  for (int j = 1; j < d.levels; ++j)
+  for (int j = 1; j < d.levels; ++j) {
+    hs_count_launches(1);
     k_sparse_level<<<blocks(n + 1), 256, 0, st>>>(lv_ptrs[j - 1], n + 1, (int64_t)1 << (j - 1), lv_ptrs[j]);
+  }
   HS_CUDA_TRY(cudaGetLastError());
 
   // ---- LCP-interval tree, best children, heavy continuations
   Sparse S{(const int32_t* const*)L.lv_ptrs, d.levels, n + 1};
   SlotMap M{L.rid, L.resp_slot, L.slot_sa_off};
   HS_CUDA_TRY(cudaMemsetAsync(L.node_flags, 0, n + 1, st));
+  hs_count_launches(1);
   k_nodes<<<blocks(n), 256, 0, st>>>(S, L.lcp, L.sa, L.rem, L.text, L.wsum, M, n, L.node_lb, L.node_flags,
                                      L.cand_parent, L.cand_mass, L.cand_tok);
   {
@@ -658,23 +673,30 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
     HS_CUDA_TRY(cudaMemsetAsync(L.ptr, 0xFF, sizeof(int64_t) * n, st));
   }
   int64_t nc = 2 * n;
+  hs_count_launches(1);
   k_best_mass<<<blocks(nc), 256, 0, st>>>(L.cand_parent, L.cand_mass, nc, L.best_mass);
+  hs_count_launches(1);
   k_best_tok<<<blocks(nc), 256, 0, st>>>(L.cand_parent, L.cand_mass, L.cand_tok, nc, L.best_mass, L.best_tok);
+  hs_count_launches(1);
   k_best_child<<<blocks(nc), 256, 0, st>>>(L.cand_parent, L.cand_mass, L.cand_tok, nc, n, L.best_mass,
                                            L.best_tok, L.ptr, L.node_flags);
+  hs_count_launches(1);
   k_ptr_init<<<blocks(n), 256, 0, st>>>(L.node_flags, L.node_lb, n, L.ptr);
   int jumps = ceil_log2((int64_t)max_len + 2) + 1;
   for (int j = 0; j < jumps; ++j) k_ptr_jump<<<blocks(n), 256, 0, st>>>(L.ptr, n);
+  hs_count_launches(1);
   k_heavy<<<blocks(n), 256, 0, st>>>(L.ptr, L.sa, n, L.heavy);
   HS_CUDA_TRY(cudaGetLastError());
 
   // ---- per-slot stats + n-gram group count
   HS_CUDA_TRY(cudaMemsetAsync(L.counters, 0, sizeof(unsigned long long) * (n_slots + 2), st));
+  hs_count_launches(1);
   k_slot_stats<<<blocks(n), 256, 0, st>>>(L.lcp, L.sa, L.rem, L.node_flags, M, n, L.counters);
   HS_CUDA_TRY(cudaMemcpy2DAsync(L.slot_stats, 2 * sizeof(int64_t), L.counters, sizeof(int64_t), sizeof(int64_t),
                                 n_slots, cudaMemcpyDeviceToDevice, st));
   unsigned long long* group_counter = L.counters + n_slots;
   HS_CUDA_TRY(cudaMemsetAsync(group_counter, 0, sizeof(unsigned long long), st));
+  hs_count_launches(1);
   k_count_groups<<<blocks(n), 256, 0, st>>>(L.lcp, L.sa, L.rem, n, prefix_min, prefix_max, group_counter);
   HS_CUDA_TRY(cudaGetLastError());
   unsigned long long groups = 0;
@@ -713,6 +735,7 @@ extern "C" int hs_index_build_table(HsIndexView* view, void* d_table, size_t tab
     d.key_bits = ceil_log2(n + 2);
     Layout L = make_layout(d, nullptr, SIZE_MAX, view->ws, view->ws_bytes, false);
     Sparse S{(const int32_t* const*)L.lv_ptrs, d.levels, n + 1};
+    hs_count_launches(1);
     k_table_insert<<<blocks(n), 256, 0, st>>>(S, view->lcp, view->sa, L.rem, view->text, view->wsum, view->heavy,
                                               L.rid, L.resp_slot, n, view->prefix_min, view->prefix_max, table,
                                               cap - 1);

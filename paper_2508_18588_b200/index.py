@@ -45,11 +45,8 @@ class GpuIndex:
 
     def __init__(self, slots, prefix_min: int = 3, prefix_max: int = 7, device=None, stream=None,
                  keep_workspace: bool = False):
+        """Build from host lists: slots[s] = [(tokens, reward), ...]."""
         torch = _lib.require_cuda()
-        lib = _lib.load()
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.prefix_min, self.prefix_max = int(prefix_min), int(min(prefix_max, _lib.HS_MAX_TABLE_PREFIX))
-        n_slots = len(slots)
         lens, rewards, toks, slot_resp_off = [], [], [], [0]
         for corpus in slots:
             for tokens, reward in corpus:
@@ -62,59 +59,89 @@ class GpuIndex:
                 rewards.append(reward_to_fx(reward))
                 toks.append(arr.astype(np.int32))
             slot_resp_off.append(slot_resp_off[-1] + len(corpus))
-        n_resp = len(lens)
-        resp_off = np.zeros(n_resp + 1, dtype=np.int64)
-        if n_resp:
+        resp_off = np.zeros(len(lens) + 1, dtype=np.int64)
+        if lens:
             resp_off[1:] = np.cumsum(lens)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        host_tok = torch.from_numpy(np.concatenate(toks) if toks else np.zeros(1, np.int32))
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev), torch.cuda.stream(s):
+            d_tok = host_tok.to(dev)
+        self._build(d_tok, resp_off, np.asarray(slot_resp_off, dtype=np.int64),
+                    np.asarray(rewards if rewards else [0], dtype=np.int64), prefix_min, prefix_max, dev, s,
+                    keep_workspace)
+
+    @classmethod
+    def from_arrays(cls, d_tokens, resp_off, slot_resp_off, reward_fx, prefix_min=3, prefix_max=7, stream=None,
+                    keep_workspace=False):
+        """Build from device tokens (int32, already in HBM) + small host metadata arrays."""
+        torch = _lib.require_cuda()
+        self = cls.__new__(cls)
+        s = stream if stream is not None else torch.cuda.current_stream(d_tokens.device)
+        self._build(d_tokens, np.asarray(resp_off, dtype=np.int64), np.asarray(slot_resp_off, dtype=np.int64),
+                    np.asarray(reward_fx, dtype=np.int64), prefix_min, prefix_max, d_tokens.device, s,
+                    keep_workspace)
+        return self
+
+    def _build(self, d_tok, resp_off, slot_resp_off, reward_fx, prefix_min, prefix_max, dev, s, keep_workspace):
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        self.device = dev
+        self.prefix_min, self.prefix_max = int(prefix_min), int(min(prefix_max, _lib.HS_MAX_TABLE_PREFIX))
+        n_resp = len(resp_off) - 1
+        n_slots = len(slot_resp_off) - 1
+        lens = np.diff(resp_off)
         self.n_tokens = int(resp_off[-1])
         self.n_slots = n_slots
         self._resp_off = resp_off
-        self._slot_resp_off = np.asarray(slot_resp_off, dtype=np.int64)
-        self._reward_fx = np.asarray(rewards if rewards else [0], dtype=np.int64)
-        self.max_len = int(max(lens)) if lens else 1
-        # per-slot host summaries
-        self.slot_tokens = [int(resp_off[self._slot_resp_off[s + 1]] - resp_off[self._slot_resp_off[s]])
-                            for s in range(n_slots)]
-        self.slot_root_mass_fx = []
-        for s in range(n_slots):
-            a, b = self._slot_resp_off[s], self._slot_resp_off[s + 1]
-            self.slot_root_mass_fx.append(int(sum(self._reward_fx[r] * lens[r] for r in range(a, b))))
-
+        self._slot_resp_off = slot_resp_off
+        self._reward_fx = reward_fx
+        self.max_len = int(lens.max()) if n_resp else 1
+        tok_at = resp_off[slot_resp_off]
+        self.slot_tokens = [int(x) for x in np.diff(tok_at)]
+        w = reward_fx[:n_resp].astype(object) * lens.astype(object) if n_resp else np.zeros(0, dtype=object)
+        csum = np.concatenate([[0], np.cumsum(w)]) if n_resp else np.zeros(1, dtype=object)
+        self.slot_root_mass_fx = [int(csum[slot_resp_off[i + 1]] - csum[slot_resp_off[i]]) for i in range(n_slots)]
         plan = _lib.HsIndexPlan()
         _lib.check(lib.hs_index_plan(self.n_tokens, n_resp, n_slots, self.max_len, self.prefix_min,
                                      self.prefix_max, ctypes.byref(plan)))
-        s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        with torch.cuda.device(self.device), torch.cuda.stream(s):
-            host_tok = torch.from_numpy(np.concatenate(toks) if toks else np.zeros(1, np.int32))
-            self.tokens = host_tok.to(self.device, non_blocking=False)
-            self.index_buf = torch.empty(max(plan.index_bytes, 256), dtype=torch.uint8, device=self.device)
-            ws = torch.empty(max(plan.workspace_bytes, 256), dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(dev), torch.cuda.stream(s):
+            self.tokens = d_tok
+            self.index_buf = torch.empty(max(plan.index_bytes, 256), dtype=torch.uint8, device=dev)
+            ws = torch.empty(max(plan.workspace_bytes, 256), dtype=torch.uint8, device=dev)
             self.view = _lib.HsIndexView()
             _lib.check(lib.hs_index_build(
-                self.tokens.data_ptr(), self.n_tokens, resp_off.ctypes.data, n_resp,
-                self._slot_resp_off.ctypes.data, n_slots, self._reward_fx.ctypes.data,
+                d_tok.data_ptr(), self.n_tokens, resp_off.ctypes.data, n_resp,
+                slot_resp_off.ctypes.data, n_slots, reward_fx.ctypes.data,
                 self.prefix_min, self.prefix_max, self.index_buf.data_ptr(), self.index_buf.numel(),
                 ws.data_ptr(), ws.numel(), ctypes.byref(self.view), s.cuda_stream))
             tb = ctypes.c_size_t(0)
             _lib.check(lib.hs_index_table_bytes(ctypes.byref(self.view), ctypes.byref(tb)))
-            self.table_buf = torch.empty(tb.value, dtype=torch.uint8, device=self.device)
+            self.table_buf = torch.empty(tb.value, dtype=torch.uint8, device=dev)
             _lib.check(lib.hs_index_build_table(ctypes.byref(self.view), self.table_buf.data_ptr(),
                                                 self.table_buf.numel(), s.cuda_stream))
-            s.synchronize()
-        self.node_counts = [1] * n_slots
-        if n_slots and self.n_tokens:
-            off = self.view.slot_stats - self.index_buf.data_ptr()
-            st = self.index_buf[off:off + 16 * n_slots].view(torch.int64).cpu().numpy()
-            self.node_counts = [int(st[2 * i]) for i in range(n_slots)]
-        # reference counts the root even for an empty slot
-        self.node_counts = [c if self.slot_tokens[i] else 1 for i, c in enumerate(self.node_counts)]
-        self.keep_workspace = keep_workspace
-        self.ws = ws if keep_workspace else None
-        if not keep_workspace:
-            self.view.ws = None
-            self.view.ws_bytes = 0
-        del ws
+            self._node_counts = None
+            if keep_workspace:
+                self.ws = ws
+            else:
+                # readers never touch the workspace; keep it alive until the table build has run
+                ws.record_stream(s)
+                self.ws = None
+                self.view.ws = None
+                self.view.ws_bytes = 0
         self.device_bytes = self.index_buf.numel() + self.table_buf.numel() + self.tokens.numel() * 4
+
+    @property
+    def node_counts(self):
+        """Reference-equivalent node count per slot (history.py node_count)."""
+        if self._node_counts is None:
+            counts = [1] * self.n_slots
+            if self.n_slots and self.n_tokens:
+                off = self.view.slot_stats - self.index_buf.data_ptr()
+                st = self.index_buf[off:off + 16 * self.n_slots].cpu().numpy().view(np.int64)
+                counts = [int(st[2 * i]) if self.slot_tokens[i] else 1 for i in range(self.n_slots)]
+            self._node_counts = counts
+        return self._node_counts
 
     # ------------------------------------------------------------------ lookups
     def lookup(self, slots, prefixes, windows, use_table: bool = False, stream=None):
