@@ -1,0 +1,85 @@
+/*
+ * hsmodel.h -- C-ABI of the verify-forward kernels (libhsmodel.so), sm_100a.
+ *
+ * The reference has no model: its "verify" compares drafts with a replayed
+ * ground truth (rhymesim/spec_engine.py:100-107) and its simulator charges a
+ * verify pass like a decode pass (sim.py:127-137).  These entry points are
+ * the real forward that produces that truth: truth[pos + i] := argmax of
+ * verify row i.  Qwen2-style decoder: RMSNorm, QKV with
+ * bias, RoPE, GQA causal attention over a slot-contiguous KV cache, SwiGLU
+ * MLP, tied or untied LM head with a fused argmax epilogue.
+ *
+ * Conventions: bf16 tensors are row-major with the last dim contiguous; the
+ * residual stream is fp32 [M, d]; "d_m" (optional, may be NULL) points at a
+ * device int32 holding the live row count, so launches sized for a maximum M
+ * can be captured in a CUDA graph.
+ */
+#ifndef HSMODEL_H_
+#define HSMODEL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HM_OK 0
+#define HM_ERR_INVALID (-1)
+#define HM_ERR_CUDA (-2)
+
+#define HM_EPI_STORE 0     /* out bf16 = acc (+ bias) */
+#define HM_EPI_SWIGLU 1    /* out bf16 [M, N/2] = silu(gate) * up; W rows interleaved in 64-row halves */
+#define HM_EPI_RESIDUAL 2  /* resid fp32 += acc */
+#define HM_EPI_ARGMAX 3    /* per 128-column tile (max, argmax) partials */
+
+typedef void* hm_stream_t;
+
+const char* hm_last_error(void);
+int64_t hm_launch_count(void);
+
+/* K3: Y = X . W^T on tcgen05 (bf16 in, fp32 TMEM accumulate), fused epilogue. */
+int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
+            int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
+            float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream);
+
+/* LM-head argmax: reduce the [M, n_tiles] partials of HM_EPI_ARGMAX (ties -> smallest id). */
+int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles, const int32_t* d_m,
+                     int32_t* d_out, hm_stream_t stream);
+
+/* x[M, d] fp32 = embedding[tokens[i]] */
+int hm_embed(const int32_t* d_tokens, const void* d_emb, int32_t M, int32_t d, float* d_x, const int32_t* d_m,
+             hm_stream_t stream);
+
+/* out bf16 = x * rsqrt(mean(x^2) + eps) * w  (row-local, fixed reduction order) */
+int hm_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t d, float eps, void* d_out,
+               const int32_t* d_m, hm_stream_t stream);
+
+/* RoPE (rotate-half, table cos/sin [max_pos, hd/2] fp32) on q and k of the fused
+ * qkv rows, q -> d_q [M, H, hd]; k, v -> cache[slot][kvh][pos][hd] */
+int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_row_slot, const float* d_cos,
+                      const float* d_sin, int32_t M, int32_t H, int32_t KVH, int32_t hd, void* d_q, void* d_kcache,
+                      void* d_vcache, int64_t slot_stride, int32_t max_len, const int32_t* d_m, hm_stream_t stream);
+
+/* K4: causal GQA attention for variable-length query blocks.  Sequence s owns
+ * query rows [q_off[s], q_off[s] + q_len[s]) at positions pos0[s] + i and KV
+ * slot kv_slot[s]; row i attends cache positions [0, pos0[s] + i]. */
+int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
+                 const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
+                 int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t hd, int32_t max_len,
+                 float scale, void* d_out, hm_stream_t stream);
+
+/* Verify-batch assembly for the rollout step: for each live sequence s
+ * (gen_len < target_len) rows [last generated token, draft_1..draft_k] at
+ * positions prompt_len[s] + gen_len[s] - 1 + i.  Writes q_off/q_len/pos0,
+ * per-row token/position/slot, and the live row count to d_m[0]. */
+int hm_build_verify_batch(int32_t n_seq, const int32_t* d_gen_tok, int32_t gen_stride, const int32_t* d_gen_len,
+                          const int32_t* d_target_len, const int32_t* d_prompt_len, const int32_t* d_draft_tok,
+                          int32_t draft_stride, const int32_t* d_draft_len, const int32_t* d_kv_slot,
+                          int32_t* d_tokens, int32_t* d_pos, int32_t* d_row_slot, int32_t* d_q_off,
+                          int32_t* d_q_len, int32_t* d_pos0, int32_t* d_m, hm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSMODEL_H_ */

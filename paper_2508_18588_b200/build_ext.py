@@ -17,6 +17,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 # library name -> sources
 LIBS = {
     "libhistospec.so": ["hs_index.cu", "hs_draft.cu", "hs_accept.cu"],
+    "libhsmodel.so": ["hm_ops.cu", "hm_gemm.cu", "hm_attn.cu"],
 }
 
 
@@ -25,7 +26,7 @@ def _stale(out, srcs):
         return True
     t = os.path.getmtime(out)
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    deps.append(os.path.join(ROOT, "include", "histospec.h"))
+    deps += [os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

@@ -1,0 +1,284 @@
+// K4: causal GQA attention for variable-length query blocks (decode rows,
+// verify blocks [last, d_1..d_k], prefill prompts) over a slot-contiguous KV
+// cache.  One CTA = (query tile, kv head, sequence); its 64 rows are
+// (query i, head j in the GQA group) pairs, so the group shares every K/V
+// load.  K/V blocks of 64 keys are double-buffered in XOR-swizzled smem with
+// cp.async; QK^T and PV run on mma.sync m16n8k16 bf16 with fp32 accumulate
+// and an online softmax in the exp2 domain.
+//
+// Batch invariance: a row's result depends only on its own query, its
+// position and the cache -- KV blocks are visited in the same order from
+// position 0 for every row, blocks past a row's position are fully masked
+// (exact no-ops), and there is no split-KV whose partition could move with the
+// batch composition.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/hsmodel.h"
+
+void hm_set_error(const char* msg);
+void hm_count_launches(int64_t n);
+
+namespace hm {
+
+constexpr int AT_ROWS = 64;   // rows per CTA (4 warps x 16)
+constexpr int AT_KEYS = 64;   // keys per block
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// [rows][HD] bf16 tile, 16-byte chunks XOR-swizzled by (row & 7)
+template <int HD>
+__device__ __forceinline__ int swz(int row, int chunk) {
+  return row * (HD / 8) + (chunk ^ (row & 7));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128) k_attention(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
+                                                   const __nv_bfloat16* __restrict__ vc, int64_t slot_stride,
+                                                   const int32_t* __restrict__ q_off, const int32_t* __restrict__ q_len,
+                                                   const int32_t* __restrict__ pos0, const int32_t* __restrict__ kv_slot,
+                                                   int H, int KVH, int max_len, float scale_log2,
+                                                   __nv_bfloat16* __restrict__ out) {
+  constexpr int CH = HD / 8;   // 16-byte chunks per row
+  const int tile = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+  const int G = H / KVH;
+  const int ql = q_len[s];
+  const int rows_total = ql * G;
+  if (tile * AT_ROWS >= rows_total) return;
+  const int qo = q_off[s], p0 = pos0[s];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint4* sQ = reinterpret_cast<uint4*>(sm);                       // [64][HD]
+  uint4* sK = sQ + AT_ROWS * CH;                                    // [2][64][HD]
+  uint4* sV = sK + 2 * AT_KEYS * CH;                                // [2][64][HD]
+
+  // ---- stage Q rows (row r -> query r / G, head kvh * G + r % G)
+  for (int c = threadIdx.x; c < AT_ROWS * CH; c += blockDim.x) {
+    const int r = c / CH, ch = c % CH;
+    const int rr = tile * AT_ROWS + r;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (rr < rows_total) {
+      const int qi = rr / G, hj = kvh * G + rr % G;
+      v = reinterpret_cast<const uint4*>(q + ((size_t)(qo + qi) * H + hj) * HD)[ch];
+    }
+    sQ[swz<HD>(r, ch)] = v;
+  }
+  // max position among this tile's rows
+  const int last_row = min(rows_total, (tile + 1) * AT_ROWS) - 1;
+  const int max_pos = p0 + last_row / G;
+  const int n_blocks = max_pos / AT_KEYS + 1;
+  const __nv_bfloat16* kbase = kc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
+  const __nv_bfloat16* vbase = vc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
+
+  auto load_kv = [&](int blk, int buf) {
+    for (int c = threadIdx.x; c < AT_KEYS * CH; c += blockDim.x) {
+      const int r = c / CH, ch = c % CH;
+      const int key = blk * AT_KEYS + r;
+      const bool ok = key <= max_pos;
+      const size_t off = (size_t)(ok ? key : 0) * HD + ch * 8;
+      cp_async16(&sK[buf * AT_KEYS * CH + swz<HD>(r, ch)], kbase + off, ok);
+      cp_async16(&sV[buf * AT_KEYS * CH + swz<HD>(r, ch)], vbase + off, ok);
+    }
+    cp_commit();
+  };
+  load_kv(0, 0);
+  __syncthreads();
+
+  // ---- Q fragments (A operand) for this warp's 16 rows
+  uint32_t qf[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int r = warp * 16 + (lane & 15);
+    const int ch = kk * 2 + (lane >> 4);
+    ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], &sQ[swz<HD>(r, ch)]);
+  }
+  // rows owned by this thread in the C layout
+  const int r0 = tile * AT_ROWS + warp * 16 + (lane >> 2);
+  const int r1 = r0 + 8;
+  const int rpos0 = r0 < rows_total ? p0 + r0 / G : -1;   // -1 => padding row (fully masked)
+  const int rpos1 = r1 < rows_total ? p0 + r1 / G : -1;
+
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int blk = 0; blk < n_blocks; ++blk) {
+    const int buf = blk & 1;
+    if (blk + 1 < n_blocks) {
+      load_kv(blk + 1, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const uint4* K = sK + buf * AT_KEYS * CH;
+    const uint4* V = sV + buf * AT_KEYS * CH;
+    // S = Q K^T : 16 x 64 per warp (8 n-tiles of 8 keys)
+    float sc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t b0, b1, b2, b3;
+        const int key = j * 8 + (lane & 7);
+        const int ch = c * 4 + (lane >> 3);
+        ldsm_x4(b0, b1, b2, b3, &K[swz<HD>(key, ch)]);
+        mma16816(sc[j], qf[2 * c], b0, b1);
+        mma16816(sc[j], qf[2 * c + 1], b2, b3);
+      }
+    }
+    // mask + online softmax (log2 domain)
+    float bm0 = -INFINITY, bm1 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int kbase_ = blk * AT_KEYS + j * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = kbase_ + e;
+        sc[j][e] = key <= rpos0 ? sc[j][e] * scale_log2 : -INFINITY;
+        sc[j][2 + e] = key <= rpos1 ? sc[j][2 + e] * scale_log2 : -INFINITY;
+        bm0 = fmaxf(bm0, sc[j][e]);
+        bm1 = fmaxf(bm1, sc[j][2 + e]);
+      }
+    }
+    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+    const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+    const float a0 = nm0 == -INFINITY ? 1.f : exp2f(m0 - nm0);
+    const float a1 = nm1 == -INFINITY ? 1.f : exp2f(m1 - nm1);
+    const float sub0 = nm0 == -INFINITY ? 0.f : nm0;
+    const float sub1 = nm1 == -INFINITY ? 0.f : nm1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j][0] = exp2f(sc[j][0] - sub0);
+      sc[j][1] = exp2f(sc[j][1] - sub0);
+      sc[j][2] = exp2f(sc[j][2] - sub1);
+      sc[j][3] = exp2f(sc[j][3] - sub1);
+      rs0 += sc[j][0] + sc[j][1];
+      rs1 += sc[j][2] + sc[j][3];
+    }
+    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+    l0 = l0 * a0 + rs0;
+    l1 = l1 * a1 + rs1;
+    m0 = nm0;
+    m1 = nm1;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= a0;
+      o[i][1] *= a0;
+      o[i][2] *= a1;
+      o[i][3] *= a1;
+    }
+    // O += P V : P (16 x 64) as A fragments, V via transposed ldmatrix
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {   // 16 keys per k-step
+      uint32_t pa[4];
+      pa[0] = pack2(sc[2 * t][0], sc[2 * t][1]);
+      pa[1] = pack2(sc[2 * t][2], sc[2 * t][3]);
+      pa[2] = pack2(sc[2 * t + 1][0], sc[2 * t + 1][1]);
+      pa[3] = pack2(sc[2 * t + 1][2], sc[2 * t + 1][3]);
+#pragma unroll
+      for (int n = 0; n < HD / 16; ++n) {   // two 8-dim n-tiles per ldmatrix.x4
+        uint32_t b0, b1, b2, b3;
+        const int key = t * 16 + (lane & 15);
+        const int ch = n * 2 + (lane >> 4);
+        ldsm_x4_t(b0, b1, b2, b3, &V[swz<HD>(key, ch)]);
+        mma16816(o[2 * n], pa, b0, b1);
+        mma16816(o[2 * n + 1], pa, b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- normalize + store: row r -> out[(qo + r / G), head kvh * G + r % G, :]
+  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f;
+  const float inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    const int col = i * 8 + 2 * (lane & 3);
+    if (rpos0 >= 0) {
+      __nv_bfloat16* dst = out + ((size_t)(qo + r0 / G) * H + kvh * G + r0 % G) * HD + col;
+      *reinterpret_cast<uint32_t*>(dst) = pack2(o[i][0] * inv0, o[i][1] * inv0);
+    }
+    if (rpos1 >= 0) {
+      __nv_bfloat16* dst = out + ((size_t)(qo + r1 / G) * H + kvh * G + r1 % G) * HD + col;
+      *reinterpret_cast<uint32_t*>(dst) = pack2(o[i][2] * inv1, o[i][3] * inv1);
+    }
+  }
+}
+
+}  // namespace hm
+
+extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
+                            const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
+                            const int32_t* d_kv_slot, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
+                            int32_t hd, int32_t max_len, float scale, void* d_out, hm_stream_t stream) {
+  if (n_seq <= 0 || max_q_len <= 0) return HM_OK;
+  if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
+  const int G = H / KVH;
+  dim3 grid((max_q_len * G + hm::AT_ROWS - 1) / hm::AT_ROWS, KVH, n_seq);
+  const float scale_log2 = scale * 1.4426950408889634f;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (hd == 128) {
+    const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;
+    static bool set = false;
+    if (!set) { cudaFuncSetAttribute(hm::k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set = true; }
+    hm::k_attention<128><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
+                                                  (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
+                                                  d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                  (__nv_bfloat16*)d_out);
+  } else if (hd == 64) {
+    const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 64 * 2;
+    hm::k_attention<64><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
+                                                 (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
+                                                 d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                 (__nv_bfloat16*)d_out);
+  } else {
+    hm_set_error("attention: head dim must be 64 or 128");
+    return HM_ERR_INVALID;
+  }
+  hm_count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }
+  return HM_OK;
+}

@@ -1,0 +1,354 @@
+// K3: verify-forward GEMMs on tcgen05 (sm_100a).
+//
+//   Y[M, N] = X[M, K] . W[N, K]^T     (bf16 in, fp32 accumulate in TMEM)
+//
+// One CTA computes a 128 x BN tile: warp 0 drives TMA (128B-swizzled K-major
+// tiles of X and W into a kStages-deep smem ring), warp 1 allocates TMEM and a
+// single elected thread issues tcgen05.mma (M=128, N=BN, K=16) per 16-wide K
+// slice, committing each stage back to the producer; warps 2-5 drain the fp32
+// accumulator with tcgen05.ld (one TMEM lane = one output row per thread) and
+// run the fused epilogue:
+//   EPI_STORE    bf16 out (+ bias)                         QKV (bias), generic
+//   EPI_SWIGLU   silu(gate) * up, gate/up interleaved in 64-column halves
+//   EPI_RESIDUAL fp32 residual += acc                      O-proj, down-proj
+//   EPI_ARGMAX   per-row (max, first argmax) partial per N tile  LM head
+//
+// Batch invariance (needed for bit-exact greedy under speculation): every
+// output element is produced by the same fixed K-loop order whatever M is;
+// there is no split-K and no M-dependent algorithm choice.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdio>
+
+#include "../../include/hsmodel.h"
+#include "hm_ptx.cuh"
+
+void hm_set_error(const char* msg);
+void hm_count_launches(int64_t n);
+
+namespace hm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 192;    // 6 warps
+
+enum { EPI_STORE = 0, EPI_SWIGLU = 1, EPI_RESIDUAL = 2, EPI_ARGMAX = 3 };
+
+struct EpiParams {
+  int M, N, K;
+  const __nv_bfloat16* bias;   // [N] or null
+  __nv_bfloat16* out;          // STORE: [M, ldo]; SWIGLU: [M, N/2]
+  int ldo;
+  float* resid;                // RESIDUAL: [M, ldr] fp32
+  int ldr;
+  float* amax_val;             // ARGMAX: [M, n_tiles]
+  int* amax_idx;
+  int n_tiles;
+  const int* m_dev;            // optional device-side M (CUDA-graph friendly); rows >= *m_dev skipped
+};
+
+template <int BN, int kStages>
+struct Smem {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int kStages, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, EpiParams p) {
+  using S = Smem<BN, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_blk = blockIdx.x, m_blk = blockIdx.y;
+  const int M = p.m_dev ? *p.m_dev : p.M;
+  if (m_blk * BM >= M) return;   // uniform across the CTA
+  const int num_k = p.K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<BN>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmW);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t ph = (kb / kStages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* a = smem + s * S::kStageBytes;
+        uint8_t* b = a + S::kABytes;
+        mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+        tma_load_2d(&tmX, &full[s], a, kb * BK, m_blk * BM);
+        tma_load_2d(&tmW, &full[s], b, kb * BK, n_blk * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t ph = (kb / kStages) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint8_t* a = smem + s * S::kStageBytes;
+        const uint8_t* b = a + S::kABytes;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          umma_f16(tmem, smem_desc_sw128(a + k * 32), smem_desc_sw128(b + k * 32), idesc, (kb | k) != 0);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(acc_full);
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
+    const int q = warp & 3;
+    const int row = m_blk * BM + q * 32 + lane;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16);
+    const bool live = row < M;
+    if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(t_row + c, v);
+        const int col0 = n_blk * BN + c;
+        if (p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] += __bfloat162float(p.bias[col0 + i]);
+        }
+        if (live) {
+          if constexpr (EPI == EPI_STORE) {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)row * p.ldo + col0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint4 w;
+              w.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
+              w.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
+              w.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
+              w.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
+              dst[i] = w;
+            }
+          } else {
+            float4* dst = reinterpret_cast<float4*>(p.resid + (size_t)row * p.ldr + col0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float4 r = dst[i];
+              r.x += v[4 * i + 0];
+              r.y += v[4 * i + 1];
+              r.z += v[4 * i + 2];
+              r.w += v[4 * i + 3];
+              dst[i] = r;
+            }
+          }
+        }
+      }
+    } else if constexpr (EPI == EPI_SWIGLU) {
+      constexpr int H = BN / 2;
+#pragma unroll 1
+      for (int c = 0; c < H; c += 32) {
+        float g[32], u[32];
+        tmem_ld32(t_row + c, g);
+        tmem_ld32(t_row + H + c, u);
+        if (live) {
+          const int col0 = n_blk * H + c;
+          uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)row * p.ldo + col0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 w;
+            w.x = pack_bf16(silu(g[8 * i + 0]) * u[8 * i + 0], silu(g[8 * i + 1]) * u[8 * i + 1]);
+            w.y = pack_bf16(silu(g[8 * i + 2]) * u[8 * i + 2], silu(g[8 * i + 3]) * u[8 * i + 3]);
+            w.z = pack_bf16(silu(g[8 * i + 4]) * u[8 * i + 4], silu(g[8 * i + 5]) * u[8 * i + 5]);
+            w.w = pack_bf16(silu(g[8 * i + 6]) * u[8 * i + 6], silu(g[8 * i + 7]) * u[8 * i + 7]);
+            dst[i] = w;
+          }
+        }
+      }
+    } else {  // EPI_ARGMAX
+      float best = -INFINITY;
+      int bidx = 0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(t_row + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (v[i] > best) { best = v[i]; bidx = n_blk * BN + c + i; }   // strict: first max wins
+        }
+      }
+      if (live) {
+        p.amax_val[(size_t)row * p.n_tiles + n_blk] = best;
+        p.amax_idx[(size_t)row * p.n_tiles + n_blk] = bidx;
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<BN>(tmem);
+  }
+}
+
+// final argmax over the per-tile partials (tiles in column order; ties -> smallest index)
+__global__ void k_argmax_reduce(const float* __restrict__ val, const int* __restrict__ idx, int M, int n_tiles,
+                                const int* m_dev, int* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int m = m_dev ? *m_dev : M;
+  if (row >= m) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = lane; t < n_tiles; t += 32) {
+    float v = val[(size_t)row * n_tiles + t];
+    int i = idx[(size_t)row * n_tiles + t];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if (lane == 0) out[row] = bi;
+}
+
+}  // namespace hm
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// rows x cols bf16 row-major (cols contiguous), box = box_rows x 64 cols, 128B swizzle
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, int kStages, int EPI>
+int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p, cudaStream_t st) {
+  using S = hm::Smem<BN, kStages>;
+  auto kern = hm::k_gemm<BN, kStages, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess) {
+      hm_set_error("cudaFuncSetAttribute(smem) failed");
+      return HM_ERR_CUDA;
+    }
+    attr_set = true;
+  }
+  dim3 grid(p.N / BN, (p.M + hm::BM - 1) / hm::BM);
+  hm_count_launches(1);
+  kern<<<grid, hm::kThreads, S::kBytes, st>>>(mx, mw, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    hm_set_error(cudaGetErrorString(e));
+    return HM_ERR_CUDA;
+  }
+  return HM_OK;
+}
+
+}  // namespace
+
+extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
+                       int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
+                       float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (K % hm::BK != 0 || N % 128 != 0) {
+    hm_set_error("hm_gemm: K must be a multiple of 64 and N of 128");
+    return HM_ERR_INVALID;
+  }
+  CUtensorMap mx, mw;
+  if (!make_map(&mx, d_x, M, K, ldx, hm::BM) || !make_map(&mw, d_w, N, K, ldw, 128)) {
+    hm_set_error("cuTensorMapEncodeTiled failed (alignment: base 16 B, ld multiple of 8 elements)");
+    return HM_ERR_INVALID;
+  }
+  hm::EpiParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.bias = static_cast<const __nv_bfloat16*>(d_bias);
+  p.out = static_cast<__nv_bfloat16*>(d_out);
+  p.ldo = (int)ldo;
+  p.resid = d_resid;
+  p.ldr = (int)ldr;
+  p.amax_val = d_amax_val;
+  p.amax_idx = d_amax_idx;
+  p.n_tiles = N / 128;
+  p.m_dev = d_m;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (epi) {
+    case HM_EPI_STORE: return launch<128, 6, hm::EPI_STORE>(mx, mw, p, st);
+    case HM_EPI_SWIGLU: return launch<128, 6, hm::EPI_SWIGLU>(mx, mw, p, st);
+    case HM_EPI_RESIDUAL: return launch<128, 6, hm::EPI_RESIDUAL>(mx, mw, p, st);
+    case HM_EPI_ARGMAX: return launch<128, 6, hm::EPI_ARGMAX>(mx, mw, p, st);
+    default: hm_set_error("unknown epilogue"); return HM_ERR_INVALID;
+  }
+}
+
+extern "C" int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles,
+                                const int32_t* d_m, int32_t* d_out, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  int rows_per_block = 8;
+  hm_count_launches(1);
+  hm::k_argmax_reduce<<<(M + rows_per_block - 1) / rows_per_block, 256, 0, (cudaStream_t)stream>>>(
+      d_val, d_idx, M, n_tiles, d_m, d_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    hm_set_error(cudaGetErrorString(e));
+    return HM_ERR_CUDA;
+  }
+  return HM_OK;
+}

@@ -1,0 +1,220 @@
+// Memory-bound pieces of the verify forward: embedding gather, RMSNorm,
+// RoPE + KV append (K5), verify-batch assembly.  All row-local with fixed
+// reduction orders, so a row's bits do not depend on what else is batched.
+#include <cuda_bf16.h>
+#include <cstdio>
+
+#include "../../include/hsmodel.h"
+
+namespace {
+thread_local char g_err[512];
+int64_t g_launches = 0;
+}  // namespace
+
+void hm_set_error(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
+void hm_count_launches(int64_t n) { __atomic_fetch_add(&g_launches, n, __ATOMIC_RELAXED); }
+extern "C" const char* hm_last_error(void) { return g_err; }
+extern "C" int64_t hm_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+#define HM_LAUNCH_CHECK()                                 \
+  do {                                                    \
+    hm_count_launches(1);                                 \
+    cudaError_t _e = cudaGetLastError();                  \
+    if (_e != cudaSuccess) {                              \
+      hm_set_error(cudaGetErrorString(_e));               \
+      return HM_ERR_CUDA;                                 \
+    }                                                     \
+  } while (0)
+
+namespace hm {
+
+__global__ void k_embed(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb, int M, int d,
+                        const int* m_dev, float* __restrict__ x) {
+  const int row = blockIdx.x;
+  const int m = m_dev ? *m_dev : M;
+  if (row >= m) return;
+  const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(emb + (size_t)tok[row] * d);
+  float2* dst = reinterpret_cast<float2*>(x + (size_t)row * d);
+  for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+}
+
+// warp per row; each lane owns a fixed strided set of columns
+__global__ void k_rmsnorm(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int M, int d, float eps,
+                          const int* m_dev, __nv_bfloat16* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int m = m_dev ? *m_dev : M;
+  if (row >= m) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
+  float ss = 0.f;
+  for (int i = lane; i < d / 4; i += 32) {
+    float4 v = xr[i];
+    ss += v.x * v.x;
+    ss += v.y * v.y;
+    ss += v.z * v.z;
+    ss += v.w * v.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = rsqrtf(ss / (float)d + eps);
+  __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * d);
+  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(w);
+  for (int i = lane; i < d / 4; i += 32) {
+    float4 v = xr[i];
+    float2 wa = __bfloat1622float2(w2[2 * i]), wb = __bfloat1622float2(w2[2 * i + 1]);
+    orow[2 * i] = __floats2bfloat162_rn(v.x * r * wa.x, v.y * r * wa.y);
+    orow[2 * i + 1] = __floats2bfloat162_rn(v.z * r * wb.x, v.w * r * wb.y);
+  }
+}
+
+// one block per row: threads cover (H + KVH) * hd/2 rotations and KVH * hd/2 v pairs
+__global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
+                          const int32_t* __restrict__ row_slot, const float* __restrict__ cosb,
+                          const float* __restrict__ sinb, int M, int H, int KVH, int hd,
+                          __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                          int64_t slot_stride, int max_len, const int* m_dev) {
+  const int row = blockIdx.x;
+  const int m = m_dev ? *m_dev : M;
+  if (row >= m) return;
+  const int half = hd / 2;
+  const int p = pos[row];
+  const int slot = row_slot[row];
+  const __nv_bfloat16* src = qkv + (size_t)row * (H + 2 * KVH) * hd;
+  const float* c = cosb + (size_t)p * half;
+  const float* s = sinb + (size_t)p * half;
+  const int n_rot = (H + KVH) * half;
+  for (int t = threadIdx.x; t < n_rot + KVH * half; t += blockDim.x) {
+    if (t < n_rot) {
+      const int head = t / half, i = t % half;
+      const __nv_bfloat16* hsrc = src + head * hd;
+      const float a = __bfloat162float(hsrc[i]), b = __bfloat162float(hsrc[i + half]);
+      const float ra = a * c[i] - b * s[i];
+      const float rb = b * c[i] + a * s[i];
+      if (head < H) {
+        __nv_bfloat16* dst = q + ((size_t)row * H + head) * hd;
+        dst[i] = __float2bfloat16_rn(ra);
+        dst[i + half] = __float2bfloat16_rn(rb);
+      } else {
+        const int kh = head - H;
+        __nv_bfloat16* dst = kc + (size_t)slot * slot_stride + ((size_t)kh * max_len + p) * hd;
+        dst[i] = __float2bfloat16_rn(ra);
+        dst[i + half] = __float2bfloat16_rn(rb);
+      }
+    } else {
+      const int u = t - n_rot;
+      const int kh = u / half, i = (u % half) * 2;
+      const __nv_bfloat16* vsrc = src + (H + KVH + kh) * hd;
+      __nv_bfloat16* dst = vc + (size_t)slot * slot_stride + ((size_t)kh * max_len + p) * hd;
+      dst[i] = vsrc[i];
+      dst[i + 1] = vsrc[i + 1];
+    }
+  }
+}
+
+// single block: q_len = live ? 1 + draft_len : 0; exclusive scan -> q_off; rows
+__global__ void k_build_verify(int n_seq, const int32_t* __restrict__ gen_tok, int gen_stride,
+                               const int32_t* __restrict__ gen_len, const int32_t* __restrict__ target_len,
+                               const int32_t* __restrict__ prompt_len, const int32_t* __restrict__ draft_tok,
+                               int draft_stride, const int32_t* __restrict__ draft_len,
+                               const int32_t* __restrict__ kv_slot, int32_t* __restrict__ tokens,
+                               int32_t* __restrict__ pos, int32_t* __restrict__ row_slot, int32_t* __restrict__ q_off,
+                               int32_t* __restrict__ q_len, int32_t* __restrict__ pos0, int32_t* __restrict__ m_out) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int base = 0; base < n_seq; base += blockDim.x) {
+    const int s = base + threadIdx.x;
+    int q = 0;
+    if (s < n_seq) {
+      const bool live = gen_len[s] < target_len[s] && gen_len[s] > 0;
+      q = live ? 1 + draft_len[s] : 0;
+    }
+    // block-wide exclusive scan of q
+    int incl = q;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+      int iv = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, iv, o);
+        if (lane >= o) iv += y;
+      }
+      if (lane < nw) warp_sums[lane] = iv - v;
+    }
+    __syncthreads();
+    const int off = carry + warp_sums[wid] + incl - q;
+    if (s < n_seq) {
+      q_off[s] = off;
+      q_len[s] = q;
+      const int g = gen_len[s];
+      const int p0 = prompt_len[s] + g - 1;
+      pos0[s] = p0;
+      for (int i = 0; i < q; ++i) {
+        tokens[off + i] = i == 0 ? gen_tok[(size_t)s * gen_stride + g - 1] : draft_tok[(size_t)s * draft_stride + i - 1];
+        pos[off + i] = p0 + i;
+        row_slot[off + i] = kv_slot[s];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = off + q;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) m_out[0] = carry;
+}
+
+}  // namespace hm
+
+extern "C" int hm_embed(const int32_t* d_tokens, const void* d_emb, int32_t M, int32_t d, float* d_x,
+                        const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  hm::k_embed<<<M, 128, 0, (cudaStream_t)stream>>>(d_tokens, (const __nv_bfloat16*)d_emb, M, d, d_m, d_x);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t d, float eps, void* d_out,
+                          const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (d % 4) { hm_set_error("rmsnorm: d % 4"); return HM_ERR_INVALID; }
+  const int rows = 8;
+  hm::k_rmsnorm<<<(M + rows - 1) / rows, 32 * rows, 0, (cudaStream_t)stream>>>(
+      d_x, (const __nv_bfloat16*)d_w, M, d, eps, d_m, (__nv_bfloat16*)d_out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_row_slot,
+                                 const float* d_cos, const float* d_sin, int32_t M, int32_t H, int32_t KVH,
+                                 int32_t hd, void* d_q, void* d_kcache, void* d_vcache, int64_t slot_stride,
+                                 int32_t max_len, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  hm::k_rope_kv<<<M, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_qkv, d_pos, d_row_slot, d_cos, d_sin,
+                                                     M, H, KVH, hd, (__nv_bfloat16*)d_q, (__nv_bfloat16*)d_kcache,
+                                                     (__nv_bfloat16*)d_vcache, slot_stride, max_len, d_m);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_build_verify_batch(int32_t n_seq, const int32_t* d_gen_tok, int32_t gen_stride,
+                                     const int32_t* d_gen_len, const int32_t* d_target_len,
+                                     const int32_t* d_prompt_len, const int32_t* d_draft_tok, int32_t draft_stride,
+                                     const int32_t* d_draft_len, const int32_t* d_kv_slot, int32_t* d_tokens,
+                                     int32_t* d_pos, int32_t* d_row_slot, int32_t* d_q_off, int32_t* d_q_len,
+                                     int32_t* d_pos0, int32_t* d_m, hm_stream_t stream) {
+  if (n_seq <= 0) return HM_OK;
+  hm::k_build_verify<<<1, 1024, 0, (cudaStream_t)stream>>>(n_seq, d_gen_tok, gen_stride, d_gen_len, d_target_len,
+                                                           d_prompt_len, d_draft_tok, draft_stride, d_draft_len,
+                                                           d_kv_slot, d_tokens, d_pos, d_row_slot, d_q_off, d_q_len,
+                                                           d_pos0, d_m);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}

@@ -1,0 +1,167 @@
+"""Greedy HistoSpec rollout engine (one process per GPU).
+
+Replaces the reference simulator's replay loop (`sim._make_tasks` ->
+`replay_response`, rhymesim/sim.py:344-377; spec_engine.py:200-279) with real
+forward passes.  One engine iteration for every live sequence:
+
+  K2 hs_draft                      drafts from the previous epoch's index
+  hm_build_verify_batch            rows [last token, d_1..d_k] per sequence
+  verify forward (model.Forward)   tcgen05 GEMMs, attention, fused LM-head argmax
+  K6 hs_accept_greedy              LCP accept + bonus + AIMD + prefix + stats
+                                   (KV rollback = gen_len update)
+
+With speculation off the same loop decodes one token per sequence per
+iteration, so "spec on" and "spec off" differ only in the rows fed to the
+same batch-invariant kernels -- their outputs must agree bit for bit.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .model import Forward, KVCache, ModelConfig, Weights, check, lib
+from .spec_engine import SpecBatch, SpecConfig
+
+
+@dataclass
+class RolloutResult:
+    tokens: np.ndarray            # [B, T] generated response tokens
+    stats: np.ndarray             # [B, 5] total, speculated, accepted, verify, decode
+    iterations: int
+    rows: int                     # sum of verify rows over iterations (incl. prefill rows)
+    gpu_ms: float
+    tokens_per_iter: list = field(default_factory=list)
+    flops: float = 0.0
+    kv_bytes: float = 0.0
+
+    @property
+    def generated(self) -> int:
+        return int(self.stats[:, 0].sum())
+
+
+class RolloutEngine:
+    def __init__(self, cfg: ModelConfig, weights: Weights, n_slots: int, max_len: int, device,
+                 spec: SpecConfig | None = None, prefill_rows: int = 16384):
+        import torch
+        self.cfg, self.w, self.device = cfg, weights, torch.device(device)
+        self.spec = spec or SpecConfig()
+        self.n_slots, self.max_len = n_slots, max_len
+        self.cache = KVCache(cfg, n_slots, max_len + self.spec.window_max + 2, self.device)
+        self.max_q = 1 + self.spec.window_max
+        self.fwd = Forward(weights, self.cache, max(prefill_rows, n_slots * self.max_q), self.device)
+        self.prefill_rows = prefill_rows
+        i32 = dict(dtype=torch.int32, device=self.device)
+        R = self.fwd.max_rows
+        self.tokens = torch.empty(R, **i32)
+        self.pos = torch.empty(R, **i32)
+        self.row_slot = torch.empty(R, **i32)
+        self.q_off = torch.empty(n_slots, **i32)
+        self.q_len = torch.empty(n_slots, **i32)
+        self.pos0 = torch.empty(n_slots, **i32)
+        self.d_m = torch.zeros(1, **i32)
+        self.kv_slot = torch.arange(n_slots, **i32)
+
+    # -------------------------------------------------------------- phases
+    def prefill(self, prompts, state: SpecBatch):
+        """Prompt forward in chunks; the last prompt row's argmax is response token 0."""
+        import torch
+        B, P = prompts.shape
+        first = torch.empty(B, dtype=torch.int32, device=self.device)
+        per = max(1, self.prefill_rows // P)
+        rows = 0
+        for a in range(0, B, per):
+            b = min(B, a + per)
+            n = b - a
+            M = n * P
+            self.tokens[:M] = prompts[a:b].reshape(-1)
+            self.pos[:M] = torch.arange(P, dtype=torch.int32, device=self.device).repeat(n)
+            self.row_slot[:M] = self.kv_slot[a:b].repeat_interleave(P)
+            self.q_off[:n] = torch.arange(n, dtype=torch.int32, device=self.device) * P
+            self.q_len[:n] = P
+            self.pos0[:n] = 0
+            am = self.fwd.run(M, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
+                              self.kv_slot[a:b], n, P)
+            first[a:b] = am.view(n, P)[:, P - 1]
+            rows += M
+        # iteration 0 of every response: a plain decode (pos 0 < prefix length)
+        state.draft_len.zero_()
+        state.looked.zero_()
+        q_off = torch.arange(B, dtype=torch.int32, device=self.device)
+        state.accept_greedy(first, q_off)
+        return rows
+
+    def rollout(self, prompts, target_len, slots=None, index=None, speculate=True, record_tpi=False):
+        """Generate target_len[b] tokens for each prompt row b (greedy), drafting from `index`.
+
+        prompts: [B, P] int32 (host numpy or device tensor); slots[b]: history slot of b in index.
+        """
+        import torch
+        prompts = torch.as_tensor(prompts, dtype=torch.int32).to(self.device)
+        B, P = prompts.shape
+        if B > self.n_slots:
+            raise ValueError(f"batch {B} > engine slots {self.n_slots}")
+        tl = np.asarray(target_len, dtype=np.int32)
+        if P + int(tl.max()) > self.max_len:
+            raise ValueError("prompt + target exceeds max_len")
+        slots = np.zeros(B, np.int32) if slots is None else np.asarray(slots, dtype=np.int32)
+        spec_on = bool(speculate and index is not None and self.spec.enabled)
+        state = SpecBatch(slots, tl, self.spec, speculate=np.full(B, int(spec_on), np.uint8), device=self.device,
+                          max_len=int(tl.max()), record_tpi=record_tpi)
+        prompt_len = torch.full((B,), P, dtype=torch.int32, device=self.device)
+        st = torch.cuda.current_stream(self.device)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        L = lib()
+        ev0.record(st)
+        rows = self.prefill(prompts, state)
+        ctx_rows = B * P * (P + 1) / 2.0
+        iters = 1
+        while True:
+            if spec_on:
+                state.propose(index, st)
+            check(L.hm_build_verify_batch(
+                B, state.gen_tok.data_ptr(), state.gen_stride, state.gen_len.data_ptr(), state.target_len.data_ptr(),
+                prompt_len.data_ptr(), state.draft_tok.data_ptr(), state.draft_tok.shape[1],
+                state.draft_len.data_ptr(), self.kv_slot.data_ptr(), self.tokens.data_ptr(), self.pos.data_ptr(),
+                self.row_slot.data_ptr(), self.q_off.data_ptr(), self.q_len.data_ptr(), self.pos0.data_ptr(),
+                self.d_m.data_ptr(), st.cuda_stream))
+            M = int(self.d_m.item())
+            if M == 0:
+                break
+            am = self.fwd.run(M, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
+                              self.kv_slot, B, self.max_q)
+            state.accept_greedy(am, self.q_off, st)
+            rows += M
+            iters += 1
+        ev1.record(st)
+        torch.cuda.synchronize(self.device)
+        gpu_ms = ev0.elapsed_time(ev1)
+        gen = state.gen_tok[:, :int(tl.max())].cpu().numpy()
+        stats = state.stats.cpu().numpy()
+        res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms)
+        if record_tpi:
+            res.tokens_per_iter = state.tokens_per_iter()
+        return res
+
+
+def smoke():
+    """Tiny-model greedy rollout: speculation on == off, bit for bit (called by __graft_entry__.smoke)."""
+    import torch
+    from .index import GpuIndex
+    from .model import TINY
+    from .synth import mutate
+    dev = torch.device("cuda", 0)
+    w = Weights(TINY, dev, seed=0)
+    eng = RolloutEngine(TINY, w, n_slots=16, max_len=256, device=dev)
+    rng = np.random.default_rng(0)
+    prompts = rng.integers(0, TINY.vocab, size=(16, 32), dtype=np.int32)
+    base = eng.rollout(prompts, [128] * 16, speculate=False)
+    hist = [[(mutate(rng, base.tokens[b].astype(np.int64), 0.8, 128, TINY.vocab, 4.0), 1.0) for _ in range(4)]
+            for b in range(16)]
+    idx = GpuIndex(hist)
+    spec = eng.rollout(prompts, [128] * 16, slots=np.arange(16), index=idx, speculate=True)
+    assert (spec.tokens == base.tokens).all(), "speculative output differs from greedy decode"
+    assert spec.iterations < base.iterations

@@ -1,0 +1,257 @@
+"""Qwen2-style policy for the verify forward, running on the libhsmodel.so kernels.
+
+The reference has no model; this is the "policy" whose greedy
+argmax is the truth that HistoSpec drafts are verified against
+(SURVEY.md 8(a) a15).  Shapes follow public Qwen2.5 configs; weights are
+random-init (seeded) because there is no network for checkpoints.
+
+Forward (M rows = all live sequences' verify rows):
+  embed -> L x [RMSNorm -> QKV GEMM(+bias) -> RoPE + KV append -> attention
+  -> O GEMM (+= residual) -> RMSNorm -> gate/up GEMM with SwiGLU epilogue
+  -> down GEMM (+= residual)] -> RMSNorm -> LM head GEMM with argmax epilogue.
+Residual stream fp32; GEMM operands bf16; accumulators fp32 (TMEM).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+LIB_PATH = os.path.join(_lib.PKG, "libhsmodel.so")
+_P, _I32, _I64, _F32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+SIGNATURES = {
+    "hm_last_error": None,
+    "hm_launch_count": None,
+    "hm_gemm": [_I32, _P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _P, _I64, _P, _P, _P, _P],
+    "hm_argmax_reduce": [_P, _P, _I32, _I32, _P, _P, _P],
+    "hm_embed": [_P, _P, _I32, _I32, _P, _P, _P],
+    "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
+    "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
+    "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P],
+    "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+}
+EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX = 0, 1, 2, 3
+
+_lib_model = None
+_lock = threading.Lock()
+
+
+def lib():
+    global _lib_model
+    with _lock:
+        if _lib_model is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} missing: build with `python -m paper_2508_18588_b200.build_ext`")
+            L = ctypes.CDLL(LIB_PATH)
+            for name, argt in SIGNATURES.items():
+                fn = getattr(L, name)
+                if name == "hm_last_error":
+                    fn.restype, fn.argtypes = ctypes.c_char_p, []
+                elif name == "hm_launch_count":
+                    fn.restype, fn.argtypes = ctypes.c_int64, []
+                else:
+                    fn.restype, fn.argtypes = ctypes.c_int, argt
+            _lib_model = L
+    return _lib_model
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().hm_last_error().decode(errors="replace")
+        raise (ValueError if rc == -1 else RuntimeError)(f"hsmodel error {rc}: {msg}")
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    tied: bool
+    rope_theta: float = 1e6
+    eps: float = 1e-6
+    init_std: float = 0.02
+
+    @property
+    def qkv_dim(self):
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    @property
+    def kv_bytes_per_token(self):
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * 2
+
+    def param_count(self):
+        d, L = self.d_model, self.n_layers
+        body = L * (self.qkv_dim * d + self.qkv_dim + d * self.n_heads * self.head_dim + 3 * d * self.ffn + 2 * d) + d
+        emb = self.vocab * d * (1 if self.tied else 2)
+        return body + emb
+
+    def body_params(self):
+        return self.param_count() - self.vocab * self.d_model * (1 if self.tied else 2)
+
+
+TINY = ModelConfig("tiny-2L-d256", 2, 256, 4, 4, 64, 1024, 4096, True)
+QWEN25_1P5B = ModelConfig("qwen2.5-1.5b-shape", 28, 1536, 12, 2, 128, 8960, 151936, True)
+QWEN25_7B = ModelConfig("qwen2.5-7b-shape", 28, 3584, 28, 4, 128, 18944, 152064, False)
+PRESETS = {c.name: c for c in (TINY, QWEN25_1P5B, QWEN25_7B)}
+
+
+def interleave_gate_up(gate, up, tile=64):
+    """[ffn, d] x 2 -> [2*ffn, d] with 64-row gate/up halves per 128-row GEMM tile."""
+    import torch
+    f, d = gate.shape
+    g = gate.view(f // tile, tile, d)
+    u = up.view(f // tile, tile, d)
+    return torch.stack([g, u], dim=1).reshape(2 * f, d).contiguous()
+
+
+class Weights:
+    """Random-init bf16 weights on `device` (seeded, generated on the device)."""
+
+    def __init__(self, cfg: ModelConfig, device, seed: int = 0, keep_fp32_split: bool = False):
+        import torch
+        self.cfg = cfg
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        std = cfg.init_std
+
+        def rnd(*shape):
+            return (torch.randn(*shape, generator=g, device=device, dtype=torch.float32) * std).to(torch.bfloat16)
+
+        d, hd = cfg.d_model, cfg.head_dim
+        self.embed = rnd(cfg.vocab, d)
+        self.lm_head = self.embed if cfg.tied else rnd(cfg.vocab, d)
+        self.layers = []
+        for _ in range(cfg.n_layers):
+            gate, up = rnd(cfg.ffn, d), rnd(cfg.ffn, d)
+            layer = {
+                "ln1": torch.ones(d, dtype=torch.bfloat16, device=device),
+                "wqkv": rnd(cfg.qkv_dim, d),
+                "bqkv": rnd(cfg.qkv_dim),
+                "wo": rnd(d, cfg.n_heads * hd),
+                "ln2": torch.ones(d, dtype=torch.bfloat16, device=device),
+                "wgu": interleave_gate_up(gate, up),
+                "wd": rnd(d, cfg.ffn),
+            }
+            if keep_fp32_split:
+                layer["gate"], layer["up"] = gate, up
+            self.layers.append(layer)
+        self.final_ln = torch.ones(d, dtype=torch.bfloat16, device=device)
+        half = hd // 2
+        inv = 1.0 / (cfg.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / hd))
+        self._inv_freq = inv
+
+    def rope_tables(self, max_pos, device):
+        """cos/sin [max_pos, hd/2] fp32, computed in float64 on the host (same table for every backend)."""
+        import torch
+        ang = np.arange(max_pos, dtype=np.float64)[:, None] * self._inv_freq[None, :]
+        return (torch.from_numpy(np.cos(ang).astype(np.float32)).to(device),
+                torch.from_numpy(np.sin(ang).astype(np.float32)).to(device))
+
+    def nbytes(self):
+        n = self.embed.numel() * 2 + (0 if self.cfg.tied else self.lm_head.numel() * 2)
+        for L in self.layers:
+            n += sum(t.numel() * 2 for k, t in L.items() if k not in ("gate", "up"))
+        return n
+
+
+class KVCache:
+    """Slot-contiguous KV cache: [layers][k|v][slot][kv_head][pos][head_dim] bf16 (zero-initialized)."""
+
+    def __init__(self, cfg: ModelConfig, n_slots: int, max_len: int, device):
+        import torch
+        self.cfg, self.n_slots, self.max_len = cfg, n_slots, max_len
+        self.buf = torch.zeros((cfg.n_layers, 2, n_slots, cfg.n_kv_heads, max_len, cfg.head_dim),
+                               dtype=torch.bfloat16, device=device)
+        self.slot_stride = cfg.n_kv_heads * max_len * cfg.head_dim
+
+    def k(self, layer):
+        return self.buf[layer, 0]
+
+    def v(self, layer):
+        return self.buf[layer, 1]
+
+
+class Forward:
+    """Preallocated activations for up to max_rows verify rows; runs the forward."""
+
+    def __init__(self, w: Weights, cache: KVCache, max_rows: int, device):
+        import torch
+        cfg = w.cfg
+        self.w, self.cache, self.cfg, self.max_rows, self.device = w, cache, cfg, max_rows, device
+        M, d = max_rows, cfg.d_model
+        bf = dict(dtype=torch.bfloat16, device=device)
+        self.x = torch.empty((M, d), dtype=torch.float32, device=device)
+        self.h = torch.empty((M, d), **bf)
+        self.qkv = torch.empty((M, cfg.qkv_dim), **bf)
+        self.q = torch.empty((M, cfg.n_heads, cfg.head_dim), **bf)
+        self.attn = torch.empty((M, cfg.n_heads * cfg.head_dim), **bf)
+        self.act = torch.empty((M, cfg.ffn), **bf)
+        self.n_tiles = cfg.vocab // 128
+        self.amax_val = torch.empty((M, self.n_tiles), dtype=torch.float32, device=device)
+        self.amax_idx = torch.empty((M, self.n_tiles), dtype=torch.int32, device=device)
+        self.argmax = torch.empty(M, dtype=torch.int32, device=device)
+        self.cos, self.sin = w.rope_tables(cache.max_len + 64, device)
+        self.scale = 1.0 / math.sqrt(cfg.head_dim)
+
+    def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
+            logits_out=None):
+        """Full forward over M rows; returns self.argmax[:M] (int32 next-token ids).
+
+        `logits_out` (bf16 [M, V], optional, tests only) also receives the LM-head logits.
+        """
+        import torch
+        if M > self.max_rows:
+            raise ValueError(f"{M} rows > max_rows {self.max_rows}")
+        L = lib()
+        cfg, w = self.cfg, self.w
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        mp = m_dev.data_ptr() if m_dev is not None else None
+        d = cfg.d_model
+        check(L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
+        for li, layer in enumerate(w.layers):
+            check(L.hm_rmsnorm(self.x.data_ptr(), layer["ln1"].data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
+            check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M, cfg.qkv_dim, d,
+                            layer["bqkv"].data_ptr(), self.qkv.data_ptr(), cfg.qkv_dim, None, 0, None, None, mp, st))
+            check(L.hm_rope_kv_append(self.qkv.data_ptr(), pos.data_ptr(), row_slot.data_ptr(), self.cos.data_ptr(),
+                                      self.sin.data_ptr(), M, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                      self.q.data_ptr(), self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr(),
+                                      self.cache.slot_stride, self.cache.max_len, mp, st))
+            check(L.hm_attention(self.q.data_ptr(), self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr(),
+                                 self.cache.slot_stride, q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
+                                 kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
+                                 self.cache.max_len, self.scale, self.attn.data_ptr(), st))
+            hd_all = cfg.n_heads * cfg.head_dim
+            check(L.hm_gemm(EPI_RESIDUAL, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all, M, d, hd_all,
+                            None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
+            check(L.hm_rmsnorm(self.x.data_ptr(), layer["ln2"].data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
+            check(L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M, 2 * cfg.ffn, d, None,
+                            self.act.data_ptr(), cfg.ffn, None, 0, None, None, mp, st))
+            check(L.hm_gemm(EPI_RESIDUAL, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(), cfg.ffn, M, d,
+                            cfg.ffn, None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
+        check(L.hm_rmsnorm(self.x.data_ptr(), w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
+        if logits_out is not None:
+            check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
+                            logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))
+        check(L.hm_gemm(EPI_ARGMAX, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None, None, 0,
+                        None, 0, self.amax_val.data_ptr(), self.amax_idx.data_ptr(), mp, st))
+        check(L.hm_argmax_reduce(self.amax_val.data_ptr(), self.amax_idx.data_ptr(), M, self.n_tiles, mp,
+                                 self.argmax.data_ptr(), st))
+        return self.argmax[:M]
+
+    def flops(self, q_rows, ctx_rows):
+        """Algorithmic flops of one forward: 2*(P_body+V*d)*M + 4*L*H*hd*sum q*(ctx+(q+1)/2)."""
+        cfg = self.cfg
+        lin = 2 * (cfg.body_params() + cfg.vocab * cfg.d_model) * q_rows
+        return lin + 4 * cfg.n_layers * cfg.n_heads * cfg.head_dim * ctx_rows

@@ -1,0 +1,217 @@
+"""Numerics of the verify-forward kernels (libhsmodel.so) vs plain PyTorch fp32.
+
+Tolerances: GEMM outputs are bf16-rounded fp32 accumulations -> compared to
+an fp32 torch reference within 2^-7 relative + 1e-3 absolute.  Full-model
+logits (bf16 path) vs the bf16-emulating CPU restatement within 0.05 absolute
+(logit std ~0.8) and vs the plain fp32 reference within 0.25; argmax agreement
+is required wherever the reference top-2 margin exceeds that bound.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    torch.cuda.set_device(0)
+    return torch
+
+
+def _gemm(M_, epi, x, w, bias=None, out=None, resid=None, amax=None):
+    import paper_2508_18588_b200.model as Mo
+    L = Mo.lib()
+    M, K = x.shape
+    N = w.shape[0]
+    Mo.check(L.hm_gemm(epi, x.data_ptr(), K, w.data_ptr(), K, M, N, K,
+                       bias.data_ptr() if bias is not None else None,
+                       out.data_ptr() if out is not None else None, out.shape[1] if out is not None else 0,
+                       resid.data_ptr() if resid is not None else None, resid.shape[1] if resid is not None else 0,
+                       amax[0].data_ptr() if amax else None, amax[1].data_ptr() if amax else None, None, 0))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (1, 256, 128), (300, 384, 1536), (1000, 2048, 1536),
+                                   (77, 1536, 8960)])
+def test_gemm_store_bias(torch, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, 0, x, w, bias=b, out=out)
+    ref = x.float() @ w.float().T + b.float()
+    err = (out.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -7 + 1e-3).all(), float(err.max())
+
+
+def test_gemm_rows_are_batch_invariant(torch):
+    """A row's bits do not depend on M or on the other rows in its tile."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    K, N = 1536, 384
+    x = torch.randn(517, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    full = torch.empty(517, N, dtype=torch.bfloat16, device="cuda")
+    _gemm(517, 0, x, w, out=full)
+    perm = torch.randperm(517, device="cuda", generator=g)
+    for rows in (perm[:1], perm[:5], perm[:130], perm):
+        sub = x[rows].contiguous()
+        o = torch.empty(len(rows), N, dtype=torch.bfloat16, device="cuda")
+        _gemm(len(rows), 0, sub, w, out=o)
+        assert torch.equal(o, full[rows])
+
+
+def test_gemm_swiglu_residual_argmax(torch):
+    from paper_2508_18588_b200.model import interleave_gate_up
+    g = torch.Generator(device="cuda").manual_seed(5)
+    M, K, F = 333, 256, 1024
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    gate = (torch.randn(F, K, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    up = (torch.randn(F, K, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    act = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    _gemm(M, 1, x, interleave_gate_up(gate, up), out=act)
+    gr, ur = x.float() @ gate.float().T, x.float() @ up.float().T
+    ref = torch.nn.functional.silu(gr) * ur
+    assert ((act.float() - ref).abs() <= ref.abs() * 2 ** -6 + 2e-3).all()
+    # residual
+    wd = (torch.randn(K, F, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    res = torch.randn(M, K, device="cuda", generator=g)
+    res0 = res.clone()
+    _gemm(M, 2, act, wd, resid=res)
+    ref2 = res0 + act.float() @ wd.float().T
+    assert torch.allclose(res, ref2, rtol=1e-4, atol=1e-3)
+    # argmax epilogue over a 4096-vocab head
+    V = 4096
+    E = (torch.randn(V, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    nt = V // 128
+    av = torch.empty(M, nt, device="cuda")
+    ai = torch.empty(M, nt, dtype=torch.int32, device="cuda")
+    _gemm(M, 3, x, E, amax=(av, ai))
+    import paper_2508_18588_b200.model as Mo
+    out = torch.empty(M, dtype=torch.int32, device="cuda")
+    Mo.check(Mo.lib().hm_argmax_reduce(av.data_ptr(), ai.data_ptr(), M, nt, None, out.data_ptr(), 0))
+    logits = x.float() @ E.float().T
+    top2 = logits.topk(2, dim=1).values
+    sure = (top2[:, 0] - top2[:, 1]) > 1e-3
+    assert (out.long()[sure] == logits.argmax(1)[sure]).all()
+
+
+def _attn_ref(torch, q, kc, vc, seqs, H, KVH, hd):
+    outs = []
+    for (qo, ql, p0, slot) in seqs:
+        for i in range(ql):
+            pos = p0 + i
+            for h in range(H):
+                kh = h // (H // KVH)
+                k = kc[slot, kh, :pos + 1].float()
+                v = vc[slot, kh, :pos + 1].float()
+                s = (k @ q[qo + i, h].float()) / np.sqrt(hd)
+                outs.append(((qo + i, h), torch.softmax(s, 0) @ v))
+    return outs
+
+
+@pytest.mark.parametrize("H,KVH,hd", [(12, 2, 128), (4, 4, 64)])
+def test_attention_varlen_and_invariance(torch, H, KVH, hd):
+    import paper_2508_18588_b200.model as Mo
+    g = torch.Generator(device="cuda").manual_seed(11)
+    slots, max_len = 4, 400
+    kc = torch.randn(slots, KVH, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(slots, KVH, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    # (q_off, q_len, pos0, slot): a decode row, a verify block, a prefill-like block
+    seqs = [(0, 1, 70, 0), (1, 5, 129, 1), (6, 33, 300, 2), (39, 12, 0, 3)]
+    M = 51
+    q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+
+    def run(sq):
+        i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
+        out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
+        Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+                                       i32([s[0] for s in sq]).data_ptr(), i32([s[1] for s in sq]).data_ptr(),
+                                       i32([s[2] for s in sq]).data_ptr(), i32([s[3] for s in sq]).data_ptr(),
+                                       len(sq), max(s[1] for s in sq), H, KVH, hd, max_len, 1.0 / np.sqrt(hd),
+                                       out.data_ptr(), 0))
+        return out.view(M, H, hd)
+
+    out = run(seqs)
+    for (row, h), ref in _attn_ref(torch, q, kc, vc, seqs, H, KVH, hd):
+        assert torch.allclose(out[row, h].float(), ref, atol=2e-2, rtol=2e-2), (row, h)
+    # the verify block of seq 1 computed one row at a time must be bit-identical
+    for i in range(5):
+        single = run([(1 + i, 1, 129 + i, 1)])
+        assert torch.equal(single[1 + i], out[1 + i])
+
+
+def test_tiny_forward_logits_vs_reference(torch):
+    from oracle import model_ref as R
+    from paper_2508_18588_b200.model import TINY, Forward, KVCache, Weights
+    w = Weights(TINY, "cuda", seed=0)
+    W = R.weights_fp32(w)
+    rng = np.random.default_rng(0)
+    T = 48
+    toks = rng.integers(0, TINY.vocab, size=T)
+    cache = KVCache(TINY, 1, 128, "cuda")
+    f = Forward(w, cache, 256, "cuda")
+    i32 = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32)).cuda()  # noqa: E731
+    logits = torch.empty(T, TINY.vocab, dtype=torch.bfloat16, device="cuda")
+    am = f.run(T, i32(toks), i32(np.arange(T)), i32(np.zeros(T)), i32([0]), i32([T]), i32([0]), i32([0]), 1, T,
+               logits_out=logits)
+    got = logits.float().cpu()
+    emu = R.forward_logits(TINY, W, toks, emulate_bf16=True)
+    fp = R.forward_logits(TINY, W, toks, emulate_bf16=False)
+    assert (got - emu).abs().max() < 0.05, float((got - emu).abs().max())
+    assert (got - fp).abs().max() < 0.25, float((got - fp).abs().max())
+    top2 = fp.topk(2, dim=1).values
+    sure = (top2[:, 0] - top2[:, 1]) > 0.5
+    assert (am.cpu().long()[sure] == fp.argmax(1)[sure]).all()
+
+
+def test_tiny_engine_spec_equals_greedy_and_reference_replay(torch):
+    """Greedy HistoSpec output == plain greedy output (bit-exact), and the engine's
+    draft/accept profile == the reference state machine replayed on that output."""
+    from oracle import hs_oracle_c as C
+    from paper_2508_18588_b200.engine import RolloutEngine
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import TINY, Weights
+    from paper_2508_18588_b200.synth import mutate
+    w = Weights(TINY, "cuda", seed=1)
+    B, P, T = 24, 32, 200
+    eng = RolloutEngine(TINY, w, n_slots=B, max_len=P + T + 8, device="cuda")
+    rng = np.random.default_rng(1)
+    prompts = rng.integers(0, TINY.vocab, size=(B, P), dtype=np.int32)
+    base = eng.rollout(prompts, [T] * B, speculate=False, record_tpi=True)
+    assert base.iterations == T
+    hist = [[(mutate(rng, base.tokens[b].astype(np.int64), 0.7, T, TINY.vocab, 4.0), float(rng.random() < 0.5))
+             for _ in range(8)] for b in range(B)]
+    idx = GpuIndex(hist)
+    spec = eng.rollout(prompts, [T] * B, slots=np.arange(B), index=idx, speculate=True, record_tpi=True)
+    assert np.array_equal(spec.tokens, base.tokens)
+    per, st = C.replay_batch(hist, [base.tokens[b] for b in range(B)], list(range(B)))
+    assert spec.tokens_per_iter == per
+    assert (spec.stats == st).all()
+    assert spec.iterations < base.iterations
+
+
+def test_qwen_shape_engine_spec_equals_greedy(torch):
+    """Qwen2.5-1.5B shape, small batch: bit-exact spec == greedy, profile == reference replay."""
+    from oracle import hs_oracle_c as C
+    from paper_2508_18588_b200.engine import RolloutEngine
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import QWEN25_1P5B, Weights
+    from paper_2508_18588_b200.synth import mutate
+    w = Weights(QWEN25_1P5B, "cuda", seed=0)
+    B, P, T = 8, 64, 160
+    eng = RolloutEngine(QWEN25_1P5B, w, n_slots=B, max_len=P + T + 8, device="cuda")
+    rng = np.random.default_rng(2)
+    prompts = rng.integers(0, QWEN25_1P5B.vocab, size=(B, P), dtype=np.int32)
+    base = eng.rollout(prompts, [T] * B, speculate=False)
+    hist = [[(mutate(rng, base.tokens[b].astype(np.int64), 0.7, T, QWEN25_1P5B.vocab, 4.0), 1.0)
+             for _ in range(8)] for b in range(B)]
+    idx = GpuIndex(hist)
+    spec = eng.rollout(prompts, [T] * B, slots=np.arange(B), index=idx, speculate=True, record_tpi=True)
+    assert np.array_equal(spec.tokens, base.tokens)
+    per, st = C.replay_batch(hist, [base.tokens[b] for b in range(B)], list(range(B)))
+    assert spec.tokens_per_iter == per
+    # outputs are not a degenerate loop
+    distinct = len({tuple(base.tokens[b, i:i + 4]) for b in range(B) for i in range(T - 4)}) / (B * (T - 4))
+    assert distinct > 0.5, distinct
