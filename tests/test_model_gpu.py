@@ -126,11 +126,12 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
     def run(sq):
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
         out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
+        meta = [i32([s[j] for s in sq]) for j in range(4)]   # keep alive across the launch
         Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
-                                       i32([s[0] for s in sq]).data_ptr(), i32([s[1] for s in sq]).data_ptr(),
-                                       i32([s[2] for s in sq]).data_ptr(), i32([s[3] for s in sq]).data_ptr(),
-                                       len(sq), max(s[1] for s in sq), H, KVH, hd, max_len, 1.0 / np.sqrt(hd),
-                                       out.data_ptr(), 0))
+                                       meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
+                                       meta[3].data_ptr(), len(sq), max(s[1] for s in sq), H, KVH, hd, max_len,
+                                       1.0 / np.sqrt(hd), out.data_ptr(), 0))
+        torch.cuda.synchronize()
         return out.view(M, H, hd)
 
     out = run(seqs)
