@@ -313,6 +313,168 @@ def run_replay(args, dist, pk):
     return line, data
 
 
+# ------------------------------------------------------------------ rollout workload (headline)
+
+def derived_history(rng, truths, s, G, vocab):
+    """(D): G independent s-mutations (burst 4) of each prompt's current rollout; rewards Bernoulli(0.5)."""
+    from paper_2508_18588_b200.synth import mutate
+    P, T = truths.shape
+    toks = np.empty((P, G, T), dtype=np.int32)
+    rew = np.empty((P, G), dtype=np.float64)
+    for p in range(P):
+        for g in range(G):
+            toks[p, g] = mutate(rng, truths[p].astype(np.int64), s, T, vocab, 4.0)
+            rew[p, g] = 1.0 if rng.random() < 0.5 else 0.0
+    return toks, rew
+
+
+def cpu_rollout_sample(cfg, seed, prompts, T, s, G, threads, W=None):
+    """CPU fp32 rollout of the same policy (oracle/model_ref.CpuRollout), HistoSpec drafting from (D)
+    histories of the CPU model's own greedy output.  Returns tokens/s of the speculative decode phase."""
+    import torch
+    from oracle import model_ref as R
+    torch.set_num_threads(threads)
+    if W is None:
+        from paper_2508_18588_b200.model import Weights
+        w = Weights(cfg, "cuda", seed=seed)
+        W = R.weights_fp32(w, "cpu")
+        del w
+    eng = R.CpuRollout(cfg, W, prompts.shape[1] + T + 40)
+    base, _pre, dec0, it0, _, _ = eng.rollout([list(p) for p in prompts], T, None)
+    rng = np.random.default_rng([seed, 77])
+    toks, rew = derived_history(rng, np.asarray(base, dtype=np.int32), s, G, cfg.vocab)
+    hists = [[(toks[p, g], float(rew[p, g])) for g in range(G)] for p in range(len(prompts))]
+    out, pre, dec, iters, acc, ver = eng.rollout([list(p) for p in prompts], T, hists)
+    n = len(prompts) * (T - 1)    # tokens landed by the decode phase (token 0 comes from prefill)
+    return {"value": n / dec, "nonspec_value": n / dec0, "prefill_s": pre, "decode_s": dec, "iterations": iters,
+            "accepted_per_verify": acc / max(ver, 1), "same_as_greedy": out == base,
+            "sample": f"{len(prompts)} seqs x {T} tokens after a {prompts.shape[1]}-token prompt, fp32 torch on "
+                      f"{threads} threads, prefill excluded"}, W
+
+
+def run_rollout(args, dist, pk):
+    import torch
+    from paper_2508_18588_b200 import _lib
+    from paper_2508_18588_b200.engine import RolloutEngine, profile_forward
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import PRESETS, Weights
+    from paper_2508_18588_b200.model import lib as mlib
+
+    cfg = PRESETS[args.model]
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    B, S, P, T, G = args.batch, args.samples, args.prompt_len, args.length, 8
+    n_prompts = B // S
+    w = Weights(cfg, dev, seed=args.seed)
+    eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev)
+    rng = np.random.default_rng([args.seed, 1000 + dist.rank])
+    prompts = np.repeat(rng.integers(0, cfg.vocab, size=(n_prompts, P), dtype=np.int32), S, axis=0)
+    # previous epoch: plain greedy rollout of the same engine (also the speculation-off baseline)
+    base = eng.rollout(prompts, [T] * B, speculate=False)
+    nonspec_tps = B * T / (base.gpu_ms / 1e3)
+    truths = base.tokens[::S]
+    hist, rew = derived_history(rng, truths, args.similarity, G, cfg.vocab)
+    resp_off = np.arange(n_prompts * G + 1, dtype=np.int64) * T
+    slot_resp_off = np.arange(n_prompts + 1, dtype=np.int64) * G
+    reward_fx = (rew.reshape(-1) * float(1 << 32)).astype(np.int64)
+    h_prompts = torch.from_numpy(prompts).pin_memory()
+    h_hist = torch.from_numpy(hist.reshape(-1)).pin_memory()
+    out_tok = torch.empty((B, T), dtype=torch.int32).pin_memory()
+    slots = np.arange(B) // S
+    stream = torch.cuda.current_stream(dev)
+    acc = {"ms": [], "res": None, "exact": True}
+
+    def step():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d_prompts = h_prompts.to(dev, non_blocking=True)
+        d_hist = h_hist.to(dev, non_blocking=True)
+        e0.record(stream)
+        idx = GpuIndex.from_arrays(d_hist, resp_off, slot_resp_off, reward_fx)   # K1: ingest previous epoch
+        res = eng.rollout(d_prompts, [T] * B, slots=slots, index=idx, speculate=True)
+        e1.record(stream)
+        out_tok.copy_(torch.from_numpy(res.tokens))   # results already read back by rollout(); keep pinned copy
+        e1.synchronize()
+        acc["ms"].append(e0.elapsed_time(e1))
+        acc["res"] = res
+        acc["exact"] &= bool(np.array_equal(res.tokens, base.tokens))
+
+    lc0, mc0 = _lib.load().hs_launch_count(), mlib().hm_launch_count()
+    e2e_ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
+    launches = ((_lib.load().hs_launch_count() - lc0) + (mlib().hm_launch_count() - mc0)) // (
+        args.steps + args.warmup)
+    ms_dev = float(np.mean(acc["ms"][-args.steps:]))
+    ms_dev = dist.max(ms_dev)
+    res = acc["res"]
+    st = res.stats.sum(axis=0)
+    gen = B * T
+    value = dist.sum(gen) / (ms_dev / 1e3)
+    e2e = dist.sum(gen) / (e2e_ms / 1e3)
+    # step roofline (aggregate bound: max of total bytes / HBM and total flops / sustained bf16)
+    bytes_total = res.forwards * res.weight_bytes + res.kv_bytes
+    t_roof = max(bytes_total / (pk["hbm_gbs"] * 1e9), res.flops / (pk["bf16_tflops_sustained"] * 1e12))
+    # dominant kernel, timed live with CUDA events in a representative verify forward
+    live_iters = float(st[3] + st[4])
+    q_mean = max(1, int(round((res.rows - B * P) / max(live_iters - B, 1))))
+    prof, M = profile_forward(eng, B, P + T // 2, q_mean)
+    label, (k_ms, k_n) = max(prof.items(), key=lambda kv: kv[1][0])
+    shapes = eng.fwd.gemm_shapes()
+    kernels = {}
+    for lab, (ms_, n_) in prof.items():
+        ent = {"ms_per_forward": ms_, "launches": n_}
+        if lab in shapes:
+            N_, K_ = shapes[lab]
+            tf = 2.0 * M * N_ * K_ * n_ / (ms_ / 1e3) / 1e12
+            ent.update(tflops=tf, frac=tf / pk["bf16_tflops_sustained"])
+        kernels[lab] = ent
+    if label in shapes:
+        N_, K_ = shapes[label]
+        ach = 2.0 * M * N_ * K_ * k_n / (k_ms / 1e3) / 1e12
+        roof = {"kernel": label, "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": None,
+                "per_launch_flops": 2.0 * M * N_ * K_, "M": M, "N": N_, "K": K_}
+    else:   # attention: KV bytes
+        kvb = B * (P + T // 2 + q_mean) * cfg.n_kv_heads * cfg.head_dim * 2 * 2 * k_n
+        ach = kvb / (k_ms / 1e3) / 1e9
+        roof = {"kernel": label, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "traffic": None}
+    roof["peak_source"] = pk["source"] + (" sustained" if roof["unit"] == "TFLOP/s" else "")
+    distinct = len({tuple(base.tokens[b, i:i + 4]) for b in range(0, B, S) for i in range(0, T - 4, 7)})
+    distinct /= max(1, len(range(0, B, S)) * len(range(0, T - 4, 7)))
+    line = {
+        "metric": "rollout tokens/sec (greedy HistoSpec: ingest + draft + verify forward + accept)",
+        "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": e2e_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic prompts, random-init weights (seed %d), (D) history s=%.2f G=8" % (args.seed,
+                                                                                            args.similarity),
+        "config": {"workload": "configs[1]: %s, %d prompts x %d samples per wave (%d resident sequences), "
+                               "%d-token prompts, %d-token greedy rollouts, 1 wave per step" % (
+                                   cfg.name, n_prompts, S, B, P, T),
+                   "full_job": "512 prompts x 8 samples = %d waves of %d on 1 GPU" % (4096 // B, B),
+                   "parallelism": "dp%d (independent rollout workers)" % dist.world,
+                   "l2": "KV cache (%.0f GB) and weights stream far beyond the 126 MB L2" % (
+                       eng.cache.buf.numel() * 2 / 1e9)},
+        "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
+        "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
+        "acceptance_rate": float(st[2] / max(st[1], 1)),
+        "engine_iterations": res.iterations,
+        "nonspec_value": dist.sum(B * T) / dist.max(base.gpu_ms / 1e3),
+        "speedup_vs_nonspec": value / max(nonspec_tps, 1e-9) if dist.world == 1 else None,
+        "bit_exact_vs_greedy": acc["exact"],
+        "distinct_4gram_ratio": distinct,
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(h_prompts.numel() * 4 + h_hist.numel() * 4),
+                "d2h_bytes_per_step": int(out_tok.numel() * 4 + B * 5 * 8)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_wall_ms": ms_dev, "frac": t_roof * 1e3 / ms_dev,
+                          "flops": res.flops, "bytes": bytes_total, "note": "aggregate bound max(sum bytes/HBM, "
+                          "sum flops/sustained bf16) <= sum of per-forward maxima"},
+        "kernels_ms_per_forward": kernels,
+        "profiled_forward": {"seqs": B, "rows_per_seq": q_mean, "ctx": P + T // 2, "M": M},
+        "clocks": clocks,
+    }
+    return line, {"cfg": cfg, "prompts": prompts, "T": T, "w": w}
+
+
 # ------------------------------------------------------------------ lookup microbenchmark
 
 def run_lookup(args, dist, pk):
@@ -411,20 +573,28 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="replay", choices=["replay", "lookup"])
+    ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup"])
+    ap.add_argument("--model", default="qwen2.5-1.5b-shape")
+    ap.add_argument("--batch", type=int, default=1024, help="resident sequences per wave (rollout)")
+    ap.add_argument("--prompt-len", type=int, default=256)
     ap.add_argument("--prompts", type=int, default=512)
     ap.add_argument("--samples", type=int, default=8)
     ap.add_argument("--length", type=int, default=4096)
     ap.add_argument("--similarity", type=float, default=0.7)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-prompts", type=int, default=96)
+    ap.add_argument("--cpu-seqs", type=int, default=2)
+    ap.add_argument("--cpu-tokens", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
         dist = Dist("gloo")
-        line = run_reference(args, dist)
+        if args.workload == "rollout":
+            line = run_reference_rollout(args, dist)
+        else:
+            line = run_reference(args, dist)
         if line is not None:
             print(json.dumps(line), flush=True)
         dist.close()
@@ -432,17 +602,60 @@ def main():
 
     dist = Dist("nccl")
     pk = peaks()
-    if args.workload == "replay":
+    if args.workload == "rollout":
+        line, data = run_rollout(args, dist, pk)
+    elif args.workload == "replay":
         line, data = run_replay(args, dist, pk)
     else:
         line, data = run_lookup(args, dist, pk)
-    if dist.rank == 0:
-        if dist.world == 1 and not args.no_cpu_baseline and args.workload == "replay":
-            r = cpu_replay_sample(data, args.ref_prompts, os.cpu_count() or 1)
-            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        if args.workload == "replay":
+            r = cpu_replay_sample(data, args.ref_prompts, threads)
+            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": threads, "kind": "port",
                                     "sample": r["sample"]}
+        elif args.workload == "rollout":
+            r, _ = cpu_rollout_sample(data["cfg"], args.seed, data["prompts"][:args.cpu_seqs * args.samples:
+                                                                              args.samples],
+                                      args.cpu_tokens, args.similarity, 8, threads)
+            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": threads, "kind": "port",
+                                    "sample": r["sample"], "nonspec_value": r["nonspec_value"],
+                                    "accepted_per_verify": r["accepted_per_verify"]}
+        print(json.dumps(line), flush=True)
+    elif dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
+
+
+def run_reference_rollout(args, dist):
+    """Reference arm for the rollout metric: the CPU fp32 policy + oracle HistoSpec on the host cores."""
+    if dist.rank != 0:
+        return None
+    from paper_2508_18588_b200.model import PRESETS
+    threads = os.cpu_count() or 1
+    cfg = PRESETS[args.model]
+    rng = np.random.default_rng([args.seed, 1000])
+    prompts = rng.integers(0, cfg.vocab, size=(args.cpu_seqs, args.prompt_len), dtype=np.int32)
+    W = None
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r, W = cpu_rollout_sample(cfg, args.seed, prompts, args.cpu_tokens, args.similarity, 8, threads, W=W)
+        if i >= args.warmup:
+            vals.append(r)
+    value = float(np.mean([r["value"] for r in vals]))
+    return {
+        "impl": "reference", "metric": "rollout tokens/sec (greedy HistoSpec: ingest + draft + verify forward + "
+                                      "accept)",
+        "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean([r["decode_s"] for r in vals])), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic prompts, random-init weights (seed %d), (D) history s=%.2f" % (args.seed, args.similarity),
+        "config": {"workload": "configs[1] %s on host cores (bounded sample)" % cfg.name},
+        "mean_accepted_per_verify": float(np.mean([r["accepted_per_verify"] for r in vals])),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
 
 
 if __name__ == "__main__":

@@ -99,3 +99,107 @@ def greedy(cfg, W, prompt, n_new, emulate_bf16=True):
         out.append(nxt)
         seq.append(nxt)
     return out
+
+
+class CpuRollout:
+    """fp32 CPU rollout of the same policy with HistoSpec drafting (the CPU baseline / reference arm).
+
+    KV-cached incremental forward (all host threads via torch), drafts from
+    the C oracle (`hs_oracle_c.draft`, brute-force scan of the prompt's
+    history = history.py:302-333 semantics), accept = spec_engine.py:217-240.
+    """
+
+    def __init__(self, cfg, W, max_len):
+        self.cfg, self.W, self.max_len = cfg, W, max_len
+        self.cos, self.sin = rope_tables(cfg, max_len + 64)
+
+    def _forward(self, caches, blocks):
+        """blocks: list of (seq, tokens, start_pos); returns argmax per row, per block."""
+        cfg, W = self.cfg, self.W
+        H, KVH, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        toks = torch.as_tensor(np.concatenate([np.asarray(t, dtype=np.int64) for _, t, _ in blocks]))
+        pos = np.concatenate([np.arange(p0, p0 + len(t)) for _, t, p0 in blocks])
+        cos, sin = self.cos[pos][:, None, :], self.sin[pos][:, None, :]
+        x = W["embed"][toks]
+        n = x.shape[0]
+        for li, L in enumerate(W["layers"]):
+            h = rmsnorm(x, L["ln1"], cfg.eps)
+            qkv = h @ L["wqkv"].T + L["bqkv"]
+            q = rope(qkv[:, :H * hd].view(n, H, hd), cos, sin)
+            k = rope(qkv[:, H * hd:(H + KVH) * hd].view(n, KVH, hd), cos, sin)
+            v = qkv[:, (H + KVH) * hd:].view(n, KVH, hd)
+            outs, r = [], 0
+            for s, t, p0 in blocks:
+                m = len(t)
+                K, V = caches[s][li]
+                K[:, p0:p0 + m] = k[r:r + m].transpose(0, 1)
+                V[:, p0:p0 + m] = v[r:r + m].transpose(0, 1)
+                kk = K[:, :p0 + m].repeat_interleave(H // KVH, 0)
+                vv = V[:, :p0 + m].repeat_interleave(H // KVH, 0)
+                sc = torch.einsum("qhd,hkd->hqk", q[r:r + m], kk) / math.sqrt(hd)
+                mask = torch.arange(p0 + m)[None, :] > torch.arange(p0, p0 + m)[:, None]
+                sc = sc.masked_fill(mask[None], float("-inf"))
+                outs.append(torch.einsum("hqk,hkd->qhd", torch.softmax(sc, -1), vv).reshape(m, H * hd))
+                r += m
+            x = x + torch.cat(outs) @ L["wo"].T
+            h = rmsnorm(x, L["ln2"], cfg.eps)
+            x = x + (torch.nn.functional.silu(h @ L["gate"].T) * (h @ L["up"].T)) @ L["wd"].T
+        am = (rmsnorm(x, W["final_ln"], cfg.eps) @ W["lm_head"].T).argmax(-1).numpy()
+        out, r = [], 0
+        for _, t, _ in blocks:
+            out.append(am[r:r + len(t)])
+            r += len(t)
+        return out
+
+    def rollout(self, prompts, target, histories, spec_cfg=(2, 2, 32, 7, 3)):
+        """Greedy HistoSpec rollout; returns (tokens per seq, prefill_s, decode_s, iterations, accepted, verifies)."""
+        import time
+        from oracle import hs_oracle_c as C
+        cfg = self.cfg
+        B = len(prompts)
+        caches = [[(torch.zeros(cfg.n_kv_heads, self.max_len, cfg.head_dim),
+                    torch.zeros(cfg.n_kv_heads, self.max_len, cfg.head_dim)) for _ in range(cfg.n_layers)]
+                  for _ in range(B)]
+        wi, wa, wm, pi, pm = spec_cfg
+        t0 = time.perf_counter()
+        first = self._forward(caches, [(b, prompts[b], 0) for b in range(B)])
+        t1 = time.perf_counter()
+        gen = [[int(first[b][-1])] for b in range(B)]
+        win, cur = [wi] * B, [pi] * B
+        iters = acc_tot = ver = 0
+        P = [len(p) for p in prompts]
+        while any(len(g) < target for g in gen):
+            blocks, drafts = [], {}
+            for b in range(B):
+                g = gen[b]
+                if len(g) >= target:
+                    continue
+                d, found = [], False
+                looked = histories is not None and len(g) >= cur[b]
+                if looked:
+                    d, found, _ = C.draft(histories[b], g[len(g) - cur[b]:], win[b])
+                drafts[b] = (d, looked, found)
+                blocks.append((b, [g[-1]] + d, P[b] + len(g) - 1))
+            am = self._forward(caches, blocks)
+            for (b, _t, _p), row in zip(blocks, am):
+                d, looked, found = drafts[b]
+                g = gen[b]
+                rest = target - len(g)
+                if not d:
+                    g.append(int(row[0]))
+                    if looked:
+                        cur[b] = pi if found else max(cur[b] - 1, pm)
+                    continue
+                a = 0
+                while a < len(d) and a < rest and d[a] == int(row[a]):
+                    a += 1
+                g.extend(d[:min(a, rest)])
+                if len(g) < target:
+                    g.append(int(row[min(a, rest)]))
+                win[b] = min(win[b] + wa, wm) if a == len(d) else wi
+                cur[b] = pi
+                acc_tot += min(a, rest)
+                ver += 1
+            iters += 1
+        t2 = time.perf_counter()
+        return gen, t1 - t0, t2 - t1, iters, acc_tot, ver

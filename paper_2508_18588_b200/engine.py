@@ -117,7 +117,12 @@ class RolloutEngine:
         L = lib()
         ev0.record(st)
         rows = self.prefill(prompts, state)
-        ctx_rows = B * P * (P + 1) / 2.0
+        # device-side accounting for the roofline: sum over rows of (pos + 1), over sequences of (ctx + q)
+        row_ctx = torch.zeros((), dtype=torch.int64, device=self.device)
+        seq_ctx = torch.zeros((), dtype=torch.int64, device=self.device)
+        row_ctx += B * P * (P + 1) // 2
+        seq_ctx += B * P
+        pre_rows = rows
         iters = 1
         while True:
             if spec_on:
@@ -131,6 +136,8 @@ class RolloutEngine:
             M = int(self.d_m.item())
             if M == 0:
                 break
+            row_ctx += (self.pos[:M].to(torch.int64) + 1).sum()
+            seq_ctx += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
             am = self.fwd.run(M, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
                               self.kv_slot, B, self.max_q)
             state.accept_greedy(am, self.q_off, st)
@@ -141,10 +148,46 @@ class RolloutEngine:
         gpu_ms = ev0.elapsed_time(ev1)
         gen = state.gen_tok[:, :int(tl.max())].cpu().numpy()
         stats = state.stats.cpu().numpy()
-        res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms)
+        cfg = self.cfg
+        flops = (2.0 * (cfg.body_params() + cfg.vocab * cfg.d_model) * rows
+                 + 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * float(row_ctx.item()))
+        kv_bytes = float(cfg.kv_bytes_per_token) * float(seq_ctx.item())
+        res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms, flops=flops,
+                            kv_bytes=kv_bytes)
+        per = max(1, self.prefill_rows // P)
+        res.forwards = (iters - 1) + (B + per - 1) // per   # decode/verify forwards + prefill chunks
+        res.weight_bytes = float(self.w.nbytes())
         if record_tpi:
             res.tokens_per_iter = state.tokens_per_iter()
         return res
+
+
+def profile_forward(engine: RolloutEngine, B: int, ctx: int, q: int):
+    """One verify forward of B sequences x q rows at context `ctx`, each launch bracketed by CUDA events.
+
+    Returns ({label: (total_ms, launches)}, M).  Used by bench.py for the
+    per-kernel roofline (times measured live, not under a profiler).
+    """
+    import torch
+    dev = engine.device
+    M = B * q
+    i32 = dict(dtype=torch.int32, device=dev)
+    tokens = torch.randint(0, engine.cfg.vocab, (M,), **i32)
+    pos = (torch.arange(q, **i32).repeat(B) + ctx)
+    row_slot = torch.arange(B, **i32).repeat_interleave(q)
+    q_off = torch.arange(B, **i32) * q
+    q_len = torch.full((B,), q, **i32)
+    pos0 = torch.full((B,), ctx, **i32)
+    kv = torch.arange(B, **i32)
+    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, q)   # warm
+    prof = []
+    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, q, prof=prof)
+    torch.cuda.synchronize(dev)
+    out = {}
+    for label, e0, e1 in prof:
+        t, n = out.get(label, (0.0, 0))
+        out[label] = (t + e0.elapsed_time(e1), n + 1)
+    return out, M
 
 
 def smoke():

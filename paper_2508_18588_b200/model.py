@@ -206,7 +206,7 @@ class Forward:
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
 
     def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
-            logits_out=None):
+            logits_out=None, prof=None):
         """Full forward over M rows; returns self.argmax[:M] (int32 next-token ids).
 
         `logits_out` (bf16 [M, V], optional, tests only) also receives the LM-head logits.
@@ -216,39 +216,68 @@ class Forward:
             raise ValueError(f"{M} rows > max_rows {self.max_rows}")
         L = lib()
         cfg, w = self.cfg, self.w
-        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        s_obj = stream or torch.cuda.current_stream(self.device)
+        st = s_obj.cuda_stream
         mp = m_dev.data_ptr() if m_dev is not None else None
         d = cfg.d_model
-        check(L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
+
+        def k(label, rc_fn):
+            # prof: list collecting (label, start, end) CUDA events around each launch
+            if prof is None:
+                check(rc_fn())
+                return
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s_obj)
+            check(rc_fn())
+            e1.record(s_obj)
+            prof.append((label, e0, e1))
+
+        k("embed", lambda: L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
+        hd_all = cfg.n_heads * cfg.head_dim
         for li, layer in enumerate(w.layers):
-            check(L.hm_rmsnorm(self.x.data_ptr(), layer["ln1"].data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
-            check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M, cfg.qkv_dim, d,
-                            layer["bqkv"].data_ptr(), self.qkv.data_ptr(), cfg.qkv_dim, None, 0, None, None, mp, st))
-            check(L.hm_rope_kv_append(self.qkv.data_ptr(), pos.data_ptr(), row_slot.data_ptr(), self.cos.data_ptr(),
-                                      self.sin.data_ptr(), M, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
-                                      self.q.data_ptr(), self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr(),
-                                      self.cache.slot_stride, self.cache.max_len, mp, st))
-            check(L.hm_attention(self.q.data_ptr(), self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr(),
-                                 self.cache.slot_stride, q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
-                                 kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim,
-                                 self.cache.max_len, self.scale, self.attn.data_ptr(), st))
-            hd_all = cfg.n_heads * cfg.head_dim
-            check(L.hm_gemm(EPI_RESIDUAL, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all, M, d, hd_all,
-                            None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
-            check(L.hm_rmsnorm(self.x.data_ptr(), layer["ln2"].data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
-            check(L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M, 2 * cfg.ffn, d, None,
-                            self.act.data_ptr(), cfg.ffn, None, 0, None, None, mp, st))
-            check(L.hm_gemm(EPI_RESIDUAL, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(), cfg.ffn, M, d,
-                            cfg.ffn, None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
-        check(L.hm_rmsnorm(self.x.data_ptr(), w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
+            kc, vc = self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr()
+            k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), layer["ln1"].data_ptr(), M, d, cfg.eps,
+                                              self.h.data_ptr(), mp, st))
+            k("gemm_qkv", lambda: L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M,
+                                            cfg.qkv_dim, d, layer["bqkv"].data_ptr(), self.qkv.data_ptr(),
+                                            cfg.qkv_dim, None, 0, None, None, mp, st))
+            k("rope_kv", lambda: L.hm_rope_kv_append(self.qkv.data_ptr(), pos.data_ptr(), row_slot.data_ptr(),
+                                                     self.cos.data_ptr(), self.sin.data_ptr(), M, cfg.n_heads,
+                                                     cfg.n_kv_heads, cfg.head_dim, self.q.data_ptr(), kc, vc,
+                                                     self.cache.slot_stride, self.cache.max_len, mp, st))
+            k("attention", lambda: L.hm_attention(self.q.data_ptr(), kc, vc, self.cache.slot_stride,
+                                                  q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
+                                                  kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
+                                                  cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
+                                                  self.attn.data_ptr(), st))
+            k("gemm_o", lambda: L.hm_gemm(EPI_RESIDUAL, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
+                                          M, d, hd_all, None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
+            k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), layer["ln2"].data_ptr(), M, d, cfg.eps,
+                                              self.h.data_ptr(), mp, st))
+            k("gemm_gate_up", lambda: L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M,
+                                                2 * cfg.ffn, d, None, self.act.data_ptr(), cfg.ffn, None, 0, None,
+                                                None, mp, st))
+            k("gemm_down", lambda: L.hm_gemm(EPI_RESIDUAL, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
+                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, self.x.data_ptr(), d, None, None,
+                                             mp, st))
+        k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(),
+                                          mp, st))
         if logits_out is not None:
             check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
                             logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))
-        check(L.hm_gemm(EPI_ARGMAX, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None, None, 0,
-                        None, 0, self.amax_val.data_ptr(), self.amax_idx.data_ptr(), mp, st))
-        check(L.hm_argmax_reduce(self.amax_val.data_ptr(), self.amax_idx.data_ptr(), M, self.n_tiles, mp,
-                                 self.argmax.data_ptr(), st))
+        k("gemm_lm_head_argmax", lambda: L.hm_gemm(EPI_ARGMAX, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M,
+                                                   cfg.vocab, d, None, None, 0, None, 0, self.amax_val.data_ptr(),
+                                                   self.amax_idx.data_ptr(), mp, st))
+        k("argmax_reduce", lambda: L.hm_argmax_reduce(self.amax_val.data_ptr(), self.amax_idx.data_ptr(), M,
+                                                      self.n_tiles, mp, self.argmax.data_ptr(), st))
         return self.argmax[:M]
+
+    def gemm_shapes(self):
+        """(label, N, K) of every GEMM in one forward (per layer ones repeated n_layers times)."""
+        cfg = self.cfg
+        d, hd_all = cfg.d_model, cfg.n_heads * cfg.head_dim
+        return {"gemm_qkv": (cfg.qkv_dim, d), "gemm_o": (d, hd_all), "gemm_gate_up": (2 * cfg.ffn, d),
+                "gemm_down": (d, cfg.ffn), "gemm_lm_head_argmax": (cfg.vocab, d)}
 
     def flops(self, q_rows, ctx_rows):
         """Algorithmic flops of one forward: 2*(P_body+V*d)*M + 4*L*H*hd*sum q*(ctx+(q+1)/2)."""
