@@ -29,7 +29,7 @@ extern "C" {
 #define HM_ERR_CUDA (-2)
 
 #define HM_EPI_STORE 0     /* out bf16 = acc (+ bias) */
-#define HM_EPI_SWIGLU 1    /* out bf16 [M, N/2] = silu(gate) * up; W rows interleaved in 64-row halves */
+#define HM_EPI_SWIGLU 1    /* out bf16 [M, N/2] = silu(gate) * up; W rows interleaved in hm_gemm_bn(N)/2 halves */
 #define HM_EPI_RESIDUAL 2  /* resid fp32 += acc */
 #define HM_EPI_ARGMAX 3    /* per 128-column tile (max, argmax) partials */
 
@@ -42,6 +42,9 @@ int64_t hm_launch_count(void);
 int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
             int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
             float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream);
+
+/* GEMM tile width chosen for an N (a function of N only, never of M). */
+int hm_gemm_bn(int32_t n);
 
 /* LM-head argmax: reduce the [M, n_tiles] partials of HM_EPI_ARGMAX (ties -> smallest id). */
 int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles, const int32_t* d_m,

@@ -25,13 +25,15 @@ def _r(x, on):
 
 def weights_fp32(w, device="cpu"):
     """Copy a model.Weights (bf16, any device) to fp32 tensors with split gate/up."""
+    from paper_2508_18588_b200.model import swiglu_half
     cfg = w.cfg
     out = {"embed": w.embed.float().to(device), "lm_head": w.lm_head.float().to(device),
            "final_ln": w.final_ln.float().to(device), "layers": []}
+    half = swiglu_half(cfg.ffn)
     for L in w.layers:
         wgu = L["wgu"].float().to(device)
         f = cfg.ffn
-        t = wgu.view(f // 64, 2, 64, cfg.d_model)
+        t = wgu.view(f // half, 2, half, cfg.d_model)
         out["layers"].append({
             "ln1": L["ln1"].float().to(device), "wqkv": L["wqkv"].float().to(device),
             "bqkv": L["bqkv"].float().to(device), "wo": L["wo"].float().to(device),

@@ -1,21 +1,28 @@
-// K3: verify-forward GEMMs on tcgen05 (sm_100a).
+// K3: verify-forward GEMMs on tcgen05 (sm_100a), persistent and warp-specialized.
 //
 //   Y[M, N] = X[M, K] . W[N, K]^T     (bf16 in, fp32 accumulate in TMEM)
 //
-// One CTA computes a 128 x BN tile: warp 0 drives TMA (128B-swizzled K-major
-// tiles of X and W into a kStages-deep smem ring), warp 1 allocates TMEM and a
-// single elected thread issues tcgen05.mma (M=128, N=BN, K=16) per 16-wide K
-// slice, committing each stage back to the producer; warps 2-5 drain the fp32
-// accumulator with tcgen05.ld (one TMEM lane = one output row per thread) and
-// run the fused epilogue:
+// grid = #SMs; each CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// (m fastest, so concurrently running CTAs share the W tile in L2).
+//   warp 0      TMA producer: 128B-swizzled K-major tiles of X and W into a
+//               kStages-deep smem ring (full/empty mbarriers)
+//   warp 1      TMEM owner + MMA issuer: one elected thread issues
+//               tcgen05.mma (M=128, N=BN, K=16) per 16-wide K slice into one of
+//               two TMEM accumulators, commits each smem stage back to the
+//               producer and each finished accumulator to the epilogue
+//   warps 2-5   epilogue: tcgen05.ld (TMEM lane = output row), fused op,
+//               global store, then release the accumulator -- overlapping the
+//               next tile's main loop
+// Fused epilogues:
 //   EPI_STORE    bf16 out (+ bias)                         QKV (bias), generic
-//   EPI_SWIGLU   silu(gate) * up, gate/up interleaved in 64-column halves
+//   EPI_SWIGLU   silu(gate) * up, W rows interleaved in BN/2 halves
 //   EPI_RESIDUAL fp32 residual += acc                      O-proj, down-proj
-//   EPI_ARGMAX   per-row (max, first argmax) partial per N tile  LM head
+//   EPI_ARGMAX   per-row (max, first argmax) partial per 128-column tile
 //
-// Batch invariance (needed for bit-exact greedy under speculation): every
-// output element is produced by the same fixed K-loop order whatever M is;
-// there is no split-K and no M-dependent algorithm choice.
+// Batch invariance (bit-exact greedy under speculation): BN is a function of
+// N only, the K loop of every tile runs in the same order, there is no split-K,
+// and the live row count only decides how many tiles exist -- so a row's bits
+// never depend on M or on the other rows.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdio>
@@ -41,18 +48,19 @@ struct EpiParams {
   int ldo;
   float* resid;                // RESIDUAL: [M, ldr] fp32
   int ldr;
-  float* amax_val;             // ARGMAX: [M, n_tiles]
+  float* amax_val;             // ARGMAX: [M, N/128]
   int* amax_idx;
-  int n_tiles;
-  const int* m_dev;            // optional device-side M (CUDA-graph friendly); rows >= *m_dev skipped
+  int n_amax_tiles;
+  const int* m_dev;            // optional device-side M (CUDA-graph friendly)
 };
 
 template <int BN, int kStages>
-struct Smem {
+struct Cfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = 2 * BN;    // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
@@ -62,21 +70,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst_, const float* v) {
+  uint4* dst = reinterpret_cast<uint4*>(dst_);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 w;
+    w.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
+    w.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
+    w.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
+    w.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
+    dst[i] = w;
+  }
+}
+
 template <int BN, int kStages, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, EpiParams p) {
-  using S = Smem<BN, kStages>;
+  using C = Cfg<BN, kStages>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* acc_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = empty + kStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_blk = blockIdx.x, m_blk = blockIdx.y;
   const int M = p.m_dev ? *p.m_dev : p.M;
-  if (m_blk * BM >= M) return;   // uniform across the CTA
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = p.N / BN;
+  const int total = m_tiles * n_tiles;
+  if ((int)blockIdx.x >= total) return;   // uniform across the CTA
   const int num_k = p.K / BK;
 
   if (threadIdx.x == 0) {
@@ -84,10 +108,13 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);   // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<BN>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmX);
     tma_prefetch(&tmW);
@@ -99,124 +126,129 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (kb / kStages) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* a = smem + s * S::kStageBytes;
-        uint8_t* b = a + S::kABytes;
-        mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-        tma_load_2d(&tmX, &full[s], a, kb * BK, m_blk * BM);
-        tma_load_2d(&tmW, &full[s], b, kb * BK, n_blk * BN);
+      uint32_t it = 0;   // global k-block counter (ring position)
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m_blk = t % m_tiles, n_blk = t / m_tiles;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* a = smem + s * C::kStageBytes;
+          uint8_t* b = a + C::kABytes;
+          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+          tma_load_2d(&tmX, &full[s], a, kb * BK, m_blk * BM);
+          tma_load_2d(&tmW, &full[s], b, kb * BK, n_blk * BN);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(BM, BN);
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (kb / kStages) & 1;
-        mbar_wait(&full[s], ph);
+      uint32_t it = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const int buf = local & 1;
+        const uint32_t use = (uint32_t)(local >> 1);
+        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
-        const uint8_t* a = smem + s * S::kStageBytes;
-        const uint8_t* b = a + S::kABytes;
+        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint8_t* a = smem + s * C::kStageBytes;
+          const uint8_t* b = a + C::kABytes;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          umma_f16(tmem, smem_desc_sw128(a + k * 32), smem_desc_sw128(b + k * 32), idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16(d, smem_desc_sw128(a + k * 32), smem_desc_sw128(b + k * 32), idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&acc_full[buf]);
       }
-      umma_commit(acc_full);
     }
     __syncwarp();
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
+    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
     const int q = warp & 3;
-    const int row = m_blk * BM + q * 32 + lane;
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16);
-    const bool live = row < M;
-    if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const int m_blk = t % m_tiles, n_blk = t / m_tiles;
+      const int buf = local & 1;
+      const uint32_t use = (uint32_t)(local >> 1);
+      mbar_wait(&acc_full[buf], use & 1);
+      tc_fence_after();
+      const uint32_t t_row = tmem + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
+      const int row = m_blk * BM + q * 32 + lane;
+      const bool live = row < M;
+      if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(t_row + c, v);
-        const int col0 = n_blk * BN + c;
-        if (p.bias) {
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(t_row + c, v);
+          const int col0 = n_blk * BN + c;
+          if (p.bias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += __bfloat162float(p.bias[col0 + i]);
-        }
-        if (live) {
-          if constexpr (EPI == EPI_STORE) {
-            uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)row * p.ldo + col0);
+            for (int i = 0; i < 32; ++i) v[i] += __bfloat162float(p.bias[col0 + i]);
+          }
+          if (live) {
+            if constexpr (EPI == EPI_STORE) {
+              store_bf16x32(p.out + (size_t)row * p.ldo + col0, v);
+            } else {
+              float4* dst = reinterpret_cast<float4*>(p.resid + (size_t)row * p.ldr + col0);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              uint4 w;
-              w.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
-              w.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
-              w.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
-              w.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
-              dst[i] = w;
-            }
-          } else {
-            float4* dst = reinterpret_cast<float4*>(p.resid + (size_t)row * p.ldr + col0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float4 r = dst[i];
-              r.x += v[4 * i + 0];
-              r.y += v[4 * i + 1];
-              r.z += v[4 * i + 2];
-              r.w += v[4 * i + 3];
-              dst[i] = r;
+              for (int i = 0; i < 8; ++i) {
+                float4 r = dst[i];
+                r.x += v[4 * i + 0];
+                r.y += v[4 * i + 1];
+                r.z += v[4 * i + 2];
+                r.w += v[4 * i + 3];
+                dst[i] = r;
+              }
             }
           }
         }
-      }
-    } else if constexpr (EPI == EPI_SWIGLU) {
-      constexpr int H = BN / 2;
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        constexpr int H = BN / 2;
 #pragma unroll 1
-      for (int c = 0; c < H; c += 32) {
-        float g[32], u[32];
-        tmem_ld32(t_row + c, g);
-        tmem_ld32(t_row + H + c, u);
-        if (live) {
-          const int col0 = n_blk * H + c;
-          uint4* dst = reinterpret_cast<uint4*>(p.out + (size_t)row * p.ldo + col0);
+        for (int c = 0; c < H; c += 32) {
+          float g[32], u[32];
+          tmem_ld32(t_row + c, g);
+          tmem_ld32(t_row + H + c, u);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint4 w;
-            w.x = pack_bf16(silu(g[8 * i + 0]) * u[8 * i + 0], silu(g[8 * i + 1]) * u[8 * i + 1]);
-            w.y = pack_bf16(silu(g[8 * i + 2]) * u[8 * i + 2], silu(g[8 * i + 3]) * u[8 * i + 3]);
-            w.z = pack_bf16(silu(g[8 * i + 4]) * u[8 * i + 4], silu(g[8 * i + 5]) * u[8 * i + 5]);
-            w.w = pack_bf16(silu(g[8 * i + 6]) * u[8 * i + 6], silu(g[8 * i + 7]) * u[8 * i + 7]);
-            dst[i] = w;
+          for (int i = 0; i < 32; ++i) g[i] = silu(g[i]) * u[i];
+          if (live) store_bf16x32(p.out + (size_t)row * p.ldo + n_blk * H + c, g);
+        }
+      } else {  // EPI_ARGMAX: one partial per 128 columns
+#pragma unroll 1
+        for (int h = 0; h < BN; h += 128) {
+          float best = -INFINITY;
+          int bidx = 0;
+#pragma unroll 1
+          for (int c = h; c < h + 128; c += 32) {
+            float v[32];
+            tmem_ld32(t_row + c, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (v[i] > best) { best = v[i]; bidx = n_blk * BN + c + i; }   // strict: first max wins
+            }
+          }
+          if (live) {
+            const int tile128 = (n_blk * BN + h) / 128;
+            p.amax_val[(size_t)row * p.n_amax_tiles + tile128] = best;
+            p.amax_idx[(size_t)row * p.n_amax_tiles + tile128] = bidx;
           }
         }
       }
-    } else {  // EPI_ARGMAX
-      float best = -INFINITY;
-      int bidx = 0;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        float v[32];
-        tmem_ld32(t_row + c, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (v[i] > best) { best = v[i]; bidx = n_blk * BN + c + i; }   // strict: first max wins
-        }
-      }
-      if (live) {
-        p.amax_val[(size_t)row * p.n_tiles + n_blk] = best;
-        p.amax_idx[(size_t)row * p.n_tiles + n_blk] = bidx;
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<BN>(tmem);
+    tmem_dealloc<C::kTmemCols>(tmem);
   }
 }
 
@@ -277,21 +309,29 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int6
   return r == CUDA_SUCCESS;
 }
 
+int g_num_sms = 0;
+
 template <int BN, int kStages, int EPI>
 int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p, cudaStream_t st) {
-  using S = hm::Smem<BN, kStages>;
+  using C = hm::Cfg<BN, kStages>;
   auto kern = hm::k_gemm<BN, kStages, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) != cudaSuccess) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess) {
       hm_set_error("cudaFuncSetAttribute(smem) failed");
       return HM_ERR_CUDA;
     }
     attr_set = true;
   }
-  dim3 grid(p.N / BN, (p.M + hm::BM - 1) / hm::BM);
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = ((p.M + hm::BM - 1) / hm::BM) * (p.N / BN);
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   hm_count_launches(1);
-  kern<<<grid, hm::kThreads, S::kBytes, st>>>(mx, mw, p);
+  kern<<<grid, hm::kThreads, C::kSmemBytes, st>>>(mx, mw, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     hm_set_error(cudaGetErrorString(e));
@@ -302,6 +342,11 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
 
 }  // namespace
 
+extern "C" int hm_gemm_bn(int32_t n) {
+  // tile width is a function of N only (batch invariance): 256 when it divides N and N is wide
+  return (n % 256 == 0 && n >= 2048) ? 256 : 128;
+}
+
 extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
                        int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
                        float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream) {
@@ -310,8 +355,9 @@ extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_
     hm_set_error("hm_gemm: K must be a multiple of 64 and N of 128");
     return HM_ERR_INVALID;
   }
+  const int BN = hm_gemm_bn(N);
   CUtensorMap mx, mw;
-  if (!make_map(&mx, d_x, M, K, ldx, hm::BM) || !make_map(&mw, d_w, N, K, ldw, 128)) {
+  if (!make_map(&mx, d_x, M, K, ldx, hm::BM) || !make_map(&mw, d_w, N, K, ldw, BN)) {
     hm_set_error("cuTensorMapEncodeTiled failed (alignment: base 16 B, ld multiple of 8 elements)");
     return HM_ERR_INVALID;
   }
@@ -326,16 +372,26 @@ extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_
   p.ldr = (int)ldr;
   p.amax_val = d_amax_val;
   p.amax_idx = d_amax_idx;
-  p.n_tiles = N / 128;
+  p.n_amax_tiles = N / 128;
   p.m_dev = d_m;
   cudaStream_t st = (cudaStream_t)stream;
-  switch (epi) {
-    case HM_EPI_STORE: return launch<128, 6, hm::EPI_STORE>(mx, mw, p, st);
-    case HM_EPI_SWIGLU: return launch<128, 6, hm::EPI_SWIGLU>(mx, mw, p, st);
-    case HM_EPI_RESIDUAL: return launch<128, 6, hm::EPI_RESIDUAL>(mx, mw, p, st);
-    case HM_EPI_ARGMAX: return launch<128, 6, hm::EPI_ARGMAX>(mx, mw, p, st);
-    default: hm_set_error("unknown epilogue"); return HM_ERR_INVALID;
+  if (BN == 256) {
+    switch (epi) {
+      case HM_EPI_STORE: return launch<256, 4, hm::EPI_STORE>(mx, mw, p, st);
+      case HM_EPI_SWIGLU: return launch<256, 4, hm::EPI_SWIGLU>(mx, mw, p, st);
+      case HM_EPI_RESIDUAL: return launch<256, 4, hm::EPI_RESIDUAL>(mx, mw, p, st);
+      case HM_EPI_ARGMAX: return launch<256, 4, hm::EPI_ARGMAX>(mx, mw, p, st);
+    }
+  } else {
+    switch (epi) {
+      case HM_EPI_STORE: return launch<128, 6, hm::EPI_STORE>(mx, mw, p, st);
+      case HM_EPI_SWIGLU: return launch<128, 6, hm::EPI_SWIGLU>(mx, mw, p, st);
+      case HM_EPI_RESIDUAL: return launch<128, 6, hm::EPI_RESIDUAL>(mx, mw, p, st);
+      case HM_EPI_ARGMAX: return launch<128, 6, hm::EPI_ARGMAX>(mx, mw, p, st);
+    }
   }
+  hm_set_error("unknown epilogue");
+  return HM_ERR_INVALID;
 }
 
 extern "C" int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles,

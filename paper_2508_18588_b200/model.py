@@ -31,6 +31,7 @@ SIGNATURES = {
     "hm_launch_count": None,
     "hm_gemm": [_I32, _P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _P, _I64, _P, _P, _P, _P],
     "hm_argmax_reduce": [_P, _P, _I32, _I32, _P, _P, _P],
+    "hm_gemm_bn": [_I32],
     "hm_embed": [_P, _P, _I32, _I32, _P, _P, _P],
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
@@ -107,10 +108,21 @@ QWEN25_7B = ModelConfig("qwen2.5-7b-shape", 28, 3584, 28, 4, 128, 18944, 152064,
 PRESETS = {c.name: c for c in (TINY, QWEN25_1P5B, QWEN25_7B)}
 
 
-def interleave_gate_up(gate, up, tile=64):
-    """[ffn, d] x 2 -> [2*ffn, d] with 64-row gate/up halves per 128-row GEMM tile."""
+def gemm_bn(n: int) -> int:
+    """Mirror of hm_gemm_bn: GEMM tile width for an output width n (function of n only)."""
+    return 256 if (n % 256 == 0 and n >= 2048) else 128
+
+
+def swiglu_half(ffn: int) -> int:
+    """Gate/up interleave granularity of the fused SwiGLU GEMM (half its N tile)."""
+    return gemm_bn(2 * ffn) // 2
+
+
+def interleave_gate_up(gate, up, tile=None):
+    """[ffn, d] x 2 -> [2*ffn, d] with gate/up halves of `tile` rows per GEMM N tile."""
     import torch
     f, d = gate.shape
+    tile = swiglu_half(f) if tile is None else tile
     g = gate.view(f // tile, tile, d)
     u = up.view(f // tile, tile, d)
     return torch.stack([g, u], dim=1).reshape(2 * f, d).contiguous()
