@@ -45,8 +45,10 @@ class RolloutResult:
 
 class RolloutEngine:
     def __init__(self, cfg: ModelConfig, weights: Weights, n_slots: int, max_len: int, device,
-                 spec: SpecConfig | None = None, prefill_rows: int = 16384):
+                 spec: SpecConfig | None = None, prefill_rows: int = 16384, use_graphs: bool = True,
+                 check_every: int = 8):
         import torch
+        self.use_graphs, self.check_every = use_graphs, check_every
         self.cfg, self.w, self.device = cfg, weights, torch.device(device)
         self.spec = spec or SpecConfig()
         self.n_slots, self.max_len = n_slots, max_len
@@ -117,41 +119,62 @@ class RolloutEngine:
         L = lib()
         ev0.record(st)
         rows = self.prefill(prompts, state)
-        # device-side accounting for the roofline: sum over rows of (pos + 1), over sequences of (ctx + q)
-        row_ctx = torch.zeros((), dtype=torch.int64, device=self.device)
-        seq_ctx = torch.zeros((), dtype=torch.int64, device=self.device)
-        row_ctx += B * P * (P + 1) // 2
-        seq_ctx += B * P
-        pre_rows = rows
-        iters = 1
-        while True:
+        # device-side counters: rows, iterations, sum over rows of (pos + 1), over sequences of (ctx + q)
+        acc = torch.zeros(4, dtype=torch.int64, device=self.device)
+        acc[0] = 0
+        acc[2] = B * P * (P + 1) // 2
+        acc[3] = B * P
+        row_ids = torch.arange(self.fwd.max_rows, dtype=torch.int32, device=self.device)
+        R = min(self.fwd.max_rows, B * self.max_q)
+
+        def iteration():
+            # one engine iteration, fully device-driven (row count lives in d_m): graph-capturable
+            s = torch.cuda.current_stream(self.device)
             if spec_on:
-                state.propose(index, st)
+                state.propose(index, s)
             check(L.hm_build_verify_batch(
                 B, state.gen_tok.data_ptr(), state.gen_stride, state.gen_len.data_ptr(), state.target_len.data_ptr(),
                 prompt_len.data_ptr(), state.draft_tok.data_ptr(), state.draft_tok.shape[1],
                 state.draft_len.data_ptr(), self.kv_slot.data_ptr(), self.tokens.data_ptr(), self.pos.data_ptr(),
                 self.row_slot.data_ptr(), self.q_off.data_ptr(), self.q_len.data_ptr(), self.pos0.data_ptr(),
-                self.d_m.data_ptr(), st.cuda_stream))
-            M = int(self.d_m.item())
-            if M == 0:
-                break
-            row_ctx += (self.pos[:M].to(torch.int64) + 1).sum()
-            seq_ctx += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
-            am = self.fwd.run(M, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
-                              self.kv_slot, B, self.max_q)
-            state.accept_greedy(am, self.q_off, st)
-            rows += M
-            iters += 1
+                self.d_m.data_ptr(), s.cuda_stream))
+            m = self.d_m[0]
+            live = row_ids[:R] < m
+            acc[0] += m
+            acc[1] += (m > 0).to(torch.int64)
+            acc[2] += torch.where(live, self.pos[:R].to(torch.int64) + 1, 0).sum()
+            acc[3] += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
+            am = self.fwd.run(R, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
+                              self.kv_slot, B, self.max_q, stream=s, m_dev=self.d_m)
+            state.accept_greedy(am, self.q_off, s)
+
+        # first decode iteration eagerly (initializes kernel attributes), then replay a captured graph
+        iteration()
+        if self.use_graphs:
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(st)
+            with torch.cuda.graph(graph, stream=side):
+                iteration()
+            st.wait_stream(side)
+            run = graph.replay
+        else:
+            run = iteration
+        while int(self.d_m.item()) > 0:
+            for _ in range(self.check_every if self.use_graphs else 1):
+                run()
         ev1.record(st)
         torch.cuda.synchronize(self.device)
         gpu_ms = ev0.elapsed_time(ev1)
         gen = state.gen_tok[:, :int(tl.max())].cpu().numpy()
         stats = state.stats.cpu().numpy()
+        a = acc.cpu().numpy()
+        rows += int(a[0])
+        iters = 1 + int(a[1])
         cfg = self.cfg
         flops = (2.0 * (cfg.body_params() + cfg.vocab * cfg.d_model) * rows
-                 + 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * float(row_ctx.item()))
-        kv_bytes = float(cfg.kv_bytes_per_token) * float(seq_ctx.item())
+                 + 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * float(a[2]))
+        kv_bytes = float(cfg.kv_bytes_per_token) * float(a[3])
         res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms, flops=flops,
                             kv_bytes=kv_bytes)
         per = max(1, self.prefill_rows // P)
