@@ -398,10 +398,10 @@ def run_rollout(args, dist, pk):
         acc["res"] = res
         acc["exact"] &= bool(np.array_equal(res.tokens, base.tokens))
 
-    lc0, mc0 = _lib.load().hs_launch_count(), mlib().hm_launch_count()
+    lc0, mc0, gl0 = _lib.load().hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
     e2e_ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
-    launches = ((_lib.load().hs_launch_count() - lc0) + (mlib().hm_launch_count() - mc0)) // (
-        args.steps + args.warmup)
+    launches = ((_lib.load().hs_launch_count() - lc0) + (mlib().hm_launch_count() - mc0)
+                + (eng.graph_launches - gl0)) // (args.steps + args.warmup)
     ms_dev = float(np.mean(acc["ms"][-args.steps:]))
     ms_dev = dist.max(ms_dev)
     res = acc["res"]
@@ -510,8 +510,8 @@ def run_lookup(args, dist, pk):
 
     def launch():
         _lib.check(lib.hs_draft(ctypes.byref(idx.view), n, slot.data_ptr(), flat.data_ptr(), 1, gen_len.data_ptr(),
-                                prefix_len.data_ptr(), window.data_ptr(), spec.data_ptr(), out.data_ptr(), 32,
-                                dlen.data_ptr(), looked.data_ptr(), found.data_ptr(), stream.cuda_stream))
+                                prefix_len.data_ptr(), window.data_ptr(), spec.data_ptr(), m, m, 32, out.data_ptr(),
+                                32, dlen.data_ptr(), looked.data_ptr(), found.data_ptr(), stream.cuda_stream))
 
     ms, clocks = timed(launch, args.steps, args.warmup, dist, stream, dist.local)
     dl = int(dlen.sum().item())

@@ -116,12 +116,17 @@ int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t* d_slot,
                     const int32_t* d_window, int32_t* d_out_tok, int32_t out_stride,
                     int64_t* d_out_info, int32_t use_table, hs_stream_t stream);
 
-/* K2: batched draft proposal for the rollout step (warp per sequence).
+/* K2: batched draft proposal for the rollout step.
  * Looks up iff speculate[s] && gen_len[s] >= prefix_len[s] (spec_engine.py:210),
- * using the last prefix_len generated tokens of row s. */
+ * using the last prefix_len generated tokens of row s.  [prefix_lo, prefix_hi]
+ * and window_hi bound the values prefix_len / window can hold (SpecConfig
+ * prefix_min..prefix_init, window_max): when every such prefix length is in
+ * the n-gram table and <= 8, four sequences share a warp (8-lane groups);
+ * otherwise one warp per sequence with the SA fallback. */
 int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq,
              const int32_t* d_gen_tok, int32_t gen_stride, const int32_t* d_gen_len,
              const int32_t* d_prefix_len, const int32_t* d_window, const uint8_t* d_speculate,
+             int32_t prefix_lo, int32_t prefix_hi, int32_t window_hi,
              int32_t* d_draft_tok, int32_t draft_stride, int32_t* d_draft_len,
              uint8_t* d_looked, uint8_t* d_found, hs_stream_t stream);
 

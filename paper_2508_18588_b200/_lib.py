@@ -54,7 +54,8 @@ SIGNATURES = {
     "hs_index_table_bytes": [ctypes.POINTER(HsIndexView), ctypes.POINTER(_SZ)],
     "hs_index_build_table": [ctypes.POINTER(HsIndexView), _P, _SZ, _P],
     "hs_lookup_batch": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _I32, _P, _P, _P, _I32, _P, _I32, _P],
-    "hs_draft": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P],
+    "hs_draft": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _I32, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I32, _P,
+                 _P, _P, _P],
     "hs_accept_replay": [_I32, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _I32, _P,
                          HsSpecConfig, _P],
     "hs_accept_greedy": [_I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _I32, _P,

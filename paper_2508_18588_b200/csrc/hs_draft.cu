@@ -216,6 +216,104 @@ __global__ void __launch_bounds__(256) k_draft(HsIndexView V, int32_t n_seq, con
   }
 }
 
+// K2, 8-lane groups: four sequences per warp (4x the memory-level parallelism
+// of one warp per sequence).  Used when prefix_len <= 8 and window <= 32,
+// i.e. the whole hot path (SpecConfig defaults 7 / 32).  Within a group:
+// lane j holds prefix token j, probes table entry base + j (8 x 16 B = one
+// 128 B line), verifies a tag hit with one compare per lane + group ballot,
+// and reads/writes the draft as 4 coalesced 32 B rows (tokens j, j+8, ...).
+__global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, const int32_t* __restrict__ slot_of_seq,
+                                                const int32_t* __restrict__ gen_tok, int32_t gen_stride,
+                                                const int32_t* __restrict__ gen_len,
+                                                const int32_t* __restrict__ prefix_len,
+                                                const int32_t* __restrict__ window,
+                                                const uint8_t* __restrict__ speculate,
+                                                int32_t* __restrict__ draft_tok, int32_t draft_stride,
+                                                int32_t* __restrict__ draft_len, uint8_t* __restrict__ looked,
+                                                uint8_t* __restrict__ found) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  const unsigned gmask = 0xFFu << (g * 8);
+  int64_t s = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4 + g;
+  const bool valid = s < n_seq;
+  if (!valid) s = n_seq - 1;   // keep the whole warp converged; results discarded
+  const int32_t m = prefix_len[s], pos = gen_len[s], slot = slot_of_seq[s];
+  const int32_t win = window[s];
+  const bool look = valid && speculate[s] && slot >= 0 && pos >= m && V.table && m >= V.prefix_min &&
+                    m <= V.prefix_max;
+  int32_t pre_j = 0;
+  if (look && j < m) pre_j = gen_tok[s * (int64_t)gen_stride + pos - m + j];
+  // hash (identical in every lane of the group)
+  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
+  for (int k = 0; k < 8; ++k) {
+    int32_t t = __shfl_sync(0xffffffffu, pre_j, (g << 3) + k);
+    if (k < m) h = mix64(h ^ ((uint64_t)(uint32_t)t * 0x9E3779B97F4A7C15ULL));
+  }
+  const int32_t tag = gram_tag(h, m);
+  int32_t hit_pos = -1;
+  bool done = !look;
+  int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
+  const int64_t lo = look ? V.slot_text_off[slot] : 0, hi = look ? V.slot_text_off[slot + 1] : 0;
+  // probe loop: every group iterates until it resolves (warp-uniform trip via __any_sync)
+  while (__any_sync(0xffffffffu, !done)) {
+    HsGramEntry e;
+    e.pos = -1;
+    e.tag = 0;
+    if (!done) e = V.table[(base + j) & V.table_mask];
+    const bool empty = !done && e.pos < 0;
+    const bool cand = !done && !empty && e.tag == tag && e.pos >= lo && e.pos < hi;
+    unsigned em = (__ballot_sync(0xffffffffu, empty) & gmask) >> (g * 8);
+    unsigned cm = (__ballot_sync(0xffffffffu, cand) & gmask) >> (g * 8);
+    unsigned live = em ? ((1u << (__ffs(em) - 1)) - 1u) : 0xFFu;
+    cm &= live;
+    // verify candidates in probe order (rare: at most a couple per query)
+    while (__any_sync(0xffffffffu, cm != 0)) {
+      const int src = cm ? (g << 3) + __ffs(cm) - 1 : lane;
+      const int32_t cpos = __shfl_sync(0xffffffffu, e.pos, src);
+      bool bad = false;
+      if (cm && j < m) bad = V.text[cpos + j] != pre_j;
+      unsigned bm = (__ballot_sync(0xffffffffu, bad) & gmask);
+      if (cm) {
+        if (!bm) {
+          hit_pos = cpos;
+          cm = 0;
+          em = 1;   // resolved
+        } else {
+          cm &= cm - 1;
+        }
+      }
+    }
+    if (!done && (hit_pos >= 0 || em)) done = true;
+    base += 8;
+  }
+  const bool hit = hit_pos >= 0;
+  // draft: tokens text[hit_pos + m + r*8 + j], r = 0..3, cut at the first terminal
+  int32_t t4[4];
+  int32_t first_term = 32;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int idx = r * 8 + j;
+    t4[r] = (hit && idx < win) ? V.text[hit_pos + m + idx] : 0;
+    if (hit && idx < win && t4[r] < 0 && idx < first_term) first_term = idx;
+  }
+  // group min of first_term
+  for (int o = 4; o > 0; o >>= 1) first_term = min(first_term, __shfl_xor_sync(0xffffffffu, first_term, o));
+  const int32_t len = hit ? min(first_term, win) : 0;
+  if (valid) {
+    int32_t* out = draft_tok + s * (int64_t)draft_stride;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = r * 8 + j;
+      if (idx < len) out[idx] = t4[r];
+    }
+    if (j == 0) {
+      draft_len[s] = len;
+      looked[s] = valid && speculate[s] && slot >= 0 && pos >= m;
+      found[s] = hit;
+    }
+  }
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -241,18 +339,31 @@ extern "C" int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t
 
 extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq, const int32_t* d_gen_tok,
                         int32_t gen_stride, const int32_t* d_gen_len, const int32_t* d_prefix_len,
-                        const int32_t* d_window, const uint8_t* d_speculate, int32_t* d_draft_tok,
-                        int32_t draft_stride, int32_t* d_draft_len, uint8_t* d_looked, uint8_t* d_found,
-                        hs_stream_t stream) {
+                        const int32_t* d_window, const uint8_t* d_speculate, int32_t prefix_lo, int32_t prefix_hi,
+                        int32_t window_hi, int32_t* d_draft_tok, int32_t draft_stride, int32_t* d_draft_len,
+                        uint8_t* d_looked, uint8_t* d_found, hs_stream_t stream) {
   if (n_seq <= 0) return HS_OK;
   if (draft_stride < 1) { hs_set_error("draft_stride"); return HS_ERR_INVALID; }
   int threads = 256;
-  int64_t blocks = ((int64_t)n_seq * 32 + threads - 1) / threads;
   HsIndexView V = *view;
   if (V.n_suffix == 0) {
     // empty history: every lookup misses
     V.table = nullptr;
   }
+  // every prefix length the caller can produce is tabled and <= 8, windows <= 32: 8-lane groups
+  if (V.table && prefix_lo >= V.prefix_min && prefix_hi <= V.prefix_max && prefix_hi <= 8 && window_hi <= 32 &&
+      draft_stride >= window_hi) {
+    int64_t warps = ((int64_t)n_seq + 3) / 4;
+    int64_t blocks8 = (warps * 32 + threads - 1) / threads;
+    hs_count_launches(1);
+    k_draft8<<<(unsigned)blocks8, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
+                                                                     d_gen_len, d_prefix_len, d_window, d_speculate,
+                                                                     d_draft_tok, draft_stride, d_draft_len, d_looked,
+                                                                     d_found);
+    HS_CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+  }
+  int64_t blocks = ((int64_t)n_seq * 32 + threads - 1) / threads;
   hs_count_launches(1);
   k_draft<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
                                                                  d_gen_len, d_prefix_len, d_window, d_speculate,

@@ -27,6 +27,11 @@ from .model import Forward, KVCache, ModelConfig, Weights, check, lib
 from .spec_engine import SpecBatch, SpecConfig
 
 
+def launch_count() -> int:
+    """Kernel launches issued by this repo's two libraries so far (process-wide)."""
+    return int(_lib.load().hs_launch_count()) + int(lib().hm_launch_count())
+
+
 @dataclass
 class RolloutResult:
     tokens: np.ndarray            # [B, T] generated response tokens
@@ -49,6 +54,7 @@ class RolloutEngine:
                  check_every: int = 8):
         import torch
         self.use_graphs, self.check_every = use_graphs, check_every
+        self.graph_launches = 0   # kernels executed by graph replays (not seen by the C launch counters)
         self.cfg, self.w, self.device = cfg, weights, torch.device(device)
         self.spec = spec or SpecConfig()
         self.n_slots, self.max_len = n_slots, max_len
@@ -154,10 +160,16 @@ class RolloutEngine:
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(self.device)
             side.wait_stream(st)
+            c0 = launch_count()
             with torch.cuda.graph(graph, stream=side):
                 iteration()
+            per_iter = launch_count() - c0
+            self.graph_launches -= per_iter   # captured, not executed
             st.wait_stream(side)
-            run = graph.replay
+
+            def run():
+                graph.replay()
+                self.graph_launches += per_iter
         else:
             run = iteration
         while int(self.d_m.item()) > 0:

@@ -387,11 +387,13 @@ class SpecBatch:
             self.looked.zero_()
             self.found.zero_()
             return
+        c = self.config
         _lib.check(_lib.load().hs_draft(
             ctypes.byref(index.view), self.n, self.slots.data_ptr(), self.gen_tok.data_ptr(), self.gen_stride,
             self.gen_len.data_ptr(), self.prefix_len.data_ptr(), self.window.data_ptr(),
-            self.speculate.data_ptr(), self.draft_tok.data_ptr(), self.draft_tok.shape[1],
-            self.draft_len.data_ptr(), self.looked.data_ptr(), self.found.data_ptr(), s.cuda_stream))
+            self.speculate.data_ptr(), c.prefix_min, c.prefix_init, c.window_max, self.draft_tok.data_ptr(),
+            self.draft_tok.shape[1], self.draft_len.data_ptr(), self.looked.data_ptr(), self.found.data_ptr(),
+            s.cuda_stream))
 
     def accept_replay(self, truth, truth_stride: int, stream=None) -> None:
         """K6 with supplied truth rows [n, truth_stride]."""

@@ -94,6 +94,31 @@ def test_appendix_b_stepwise_engine(mods):
     assert b.stats.cpu().numpy().sum(axis=0).tolist() == g["stats"]
 
 
+@pytest.mark.parametrize("pi,pm,wm", [(7, 3, 32), (9, 2, 32), (5, 1, 12)])
+def test_stepwise_draft_paths_match_oracle(mods, pi, pm, wm):
+    """K2 8-lane-group path (prefixes tabled, <= 8) and warp/SA fallback path vs the C oracle."""
+    H, S = mods
+    import torch
+    from oracle import hs_oracle_c as C
+    from paper_2508_18588_b200.index import GpuIndex
+    hist, truths, slots = _appendix_b(0.8)
+    truths, slots = truths[:300], slots[:300]
+    cfg = S.SpecConfig(window_max=wm, prefix_init=pi, prefix_min=pm)
+    idx = GpuIndex(hist, prefix_min=3, prefix_max=7)
+    L = max(len(t) for t in truths)
+    truth = np.zeros((len(truths), L + 40), dtype=np.int32)
+    for i, t in enumerate(truths):
+        truth[i, :len(t)] = t
+    b = S.SpecBatch(slots, [len(t) for t in truths], cfg)
+    d_truth = torch.from_numpy(truth).cuda()
+    for _ in range(L + 1):
+        b.propose(idx)
+        b.accept_replay(d_truth, truth.shape[1])
+    per, st = C.replay_batch(hist, truths, slots, cfg=(1, cfg.window_init, cfg.window_add, wm, pi, pm))
+    assert b.tokens_per_iter() == per
+    assert (b.stats.cpu().numpy() == st).all()
+
+
 def test_accept_greedy_with_oracle_argmax(mods):
     """K6 greedy: a model whose argmax reproduces the truth lands the same profile."""
     H, S = mods
