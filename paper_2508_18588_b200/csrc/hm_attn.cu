@@ -13,6 +13,7 @@
 // batch composition.
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "../../include/hsmodel.h"
 
@@ -247,6 +248,267 @@ __global__ void __launch_bounds__(128) k_attention(const __nv_bfloat16* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// v2: KV split across the 4 warps of a CTA.  A CTA owns SL m16 row slices
+// (16*SL rows of (query, head-in-group)); each pipeline stage holds 64 keys
+// of K and V; warp w processes keys [stage*64 + 16w, +16) for all of the
+// CTA's rows with its own online-softmax state, and the 4 partial states are
+// merged in warp order at the end.  Compared with v1 this computes 16*SL
+// instead of 64 rows per key (30 live rows of a q=5 verify block on GQA-6:
+// SL=2; decode: SL=1) and keeps every warp busy.  The key->warp map depends
+// only on the key position and the merge order is fixed, so a row's result is
+// independent of the batch (bit-exact greedy under speculation).
+template <int HD, int SL>
+__global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restrict__ q,
+                                                    const __nv_bfloat16* __restrict__ kc,
+                                                    const __nv_bfloat16* __restrict__ vc, int64_t slot_stride,
+                                                    const int32_t* __restrict__ q_off,
+                                                    const int32_t* __restrict__ q_len,
+                                                    const int32_t* __restrict__ pos0,
+                                                    const int32_t* __restrict__ kv_slot, int H, int KVH,
+                                                    int max_len, float scale_log2,
+                                                    __nv_bfloat16* __restrict__ out) {
+  constexpr int CH = HD / 8;        // 16-byte chunks per row
+  constexpr int ROWS = 16 * SL;
+  constexpr int KS = 64;            // keys per stage (4 warps x 16)
+  constexpr int NST = 3;            // pipeline stages
+  const int tile = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+  const int G = H / KVH;
+  const int ql = q_len[s];
+  const int rows_total = ql * G;
+  if (tile * ROWS >= rows_total) return;
+  const int qo = q_off[s], p0 = pos0[s];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint4* sK = reinterpret_cast<uint4*>(sm);            // [NST][KS][CH]
+  uint4* sV = sK + NST * KS * CH;                        // [NST][KS][CH]
+  uint4* sQ = sV + NST * KS * CH;                        // [ROWS][CH]
+
+  for (int c = threadIdx.x; c < ROWS * CH; c += blockDim.x) {
+    const int r = c / CH, ch = c % CH;
+    const int rr = tile * ROWS + r;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (rr < rows_total) {
+      const int qi = rr / G, hj = kvh * G + rr % G;
+      v = reinterpret_cast<const uint4*>(q + ((size_t)(qo + qi) * H + hj) * HD)[ch];
+    }
+    sQ[swz<HD>(r, ch)] = v;
+  }
+  const int last_row = min(rows_total, (tile + 1) * ROWS) - 1;
+  const int max_pos = p0 + last_row / G;
+  const int n_stage = max_pos / KS + 1;
+  const __nv_bfloat16* kbase = kc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
+  const __nv_bfloat16* vbase = vc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
+
+  auto load_stage = [&](int st) {
+    const int buf = st % NST;
+    for (int c = threadIdx.x; c < KS * CH; c += blockDim.x) {
+      const int r = c / CH, ch = c % CH;
+      const int key = st * KS + r;
+      const bool ok = key <= max_pos;
+      const size_t off = (size_t)(ok ? key : 0) * HD + ch * 8;
+      cp_async16(&sK[(buf * KS) * CH + swz<HD>(r, ch)], kbase + off, ok);
+      cp_async16(&sV[(buf * KS) * CH + swz<HD>(r, ch)], vbase + off, ok);
+    }
+  };
+  __syncthreads();
+  uint32_t qf[SL][HD / 16][4];
+#pragma unroll
+  for (int sl = 0; sl < SL; ++sl) {
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int r = sl * 16 + (lane & 15);
+      const int ch = kk * 2 + (lane >> 4);
+      ldsm_x4(qf[sl][kk][0], qf[sl][kk][1], qf[sl][kk][2], qf[sl][kk][3], &sQ[swz<HD>(r, ch)]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NST - 1; ++i) {
+    if (i < n_stage) load_stage(i);
+    cp_commit();
+  }
+  int rpos[SL][2];
+#pragma unroll
+  for (int sl = 0; sl < SL; ++sl) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rr = tile * ROWS + sl * 16 + (lane >> 2) + 8 * h;
+      rpos[sl][h] = rr < rows_total ? p0 + rr / G : -1;   // -1: padding row, fully masked
+    }
+  }
+  float o[SL][HD / 8][4];
+  float mrow[SL][2], lrow[SL][2];
+#pragma unroll
+  for (int sl = 0; sl < SL; ++sl) {
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) o[sl][i][0] = o[sl][i][1] = o[sl][i][2] = o[sl][i][3] = 0.f;
+    mrow[sl][0] = mrow[sl][1] = -INFINITY;
+    lrow[sl][0] = lrow[sl][1] = 0.f;
+  }
+
+  for (int st = 0; st < n_stage; ++st) {
+    cp_wait<NST - 2>();      // stage st landed (this thread's copies)
+    __syncthreads();         // ... and everyone's; stage st-1's buffer is free again
+    if (st + NST - 1 < n_stage) load_stage(st + NST - 1);
+    cp_commit();
+    const int buf = st % NST;
+    const int key0 = st * KS + warp * 16;
+    if (key0 <= max_pos) {   // warp-uniform
+      const uint4* K = sK + (buf * KS) * CH;
+      const uint4* V = sV + (buf * KS) * CH;
+#pragma unroll
+      for (int sl = 0; sl < SL; ++sl) {
+        float sc[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t b0, b1, b2, b3;
+            const int key = warp * 16 + j * 8 + (lane & 7);
+            const int ch = c * 4 + (lane >> 3);
+            ldsm_x4(b0, b1, b2, b3, &K[swz<HD>(key, ch)]);
+            mma16816(sc[j], qf[sl][2 * c], b0, b1);
+            mma16816(sc[j], qf[sl][2 * c + 1], b2, b3);
+          }
+        }
+        float bm0 = -INFINITY, bm1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int key = key0 + j * 8 + 2 * (lane & 3) + e;
+            sc[j][e] = key <= rpos[sl][0] ? sc[j][e] * scale_log2 : -INFINITY;
+            sc[j][2 + e] = key <= rpos[sl][1] ? sc[j][2 + e] * scale_log2 : -INFINITY;
+            bm0 = fmaxf(bm0, sc[j][e]);
+            bm1 = fmaxf(bm1, sc[j][2 + e]);
+          }
+        }
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+        const float nm0 = fmaxf(mrow[sl][0], bm0), nm1 = fmaxf(mrow[sl][1], bm1);
+        const float a0 = nm0 == -INFINITY ? 1.f : exp2f(mrow[sl][0] - nm0);
+        const float a1 = nm1 == -INFINITY ? 1.f : exp2f(mrow[sl][1] - nm1);
+        const float sub0 = nm0 == -INFINITY ? 0.f : nm0;
+        const float sub1 = nm1 == -INFINITY ? 0.f : nm1;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          sc[j][0] = exp2f(sc[j][0] - sub0);
+          sc[j][1] = exp2f(sc[j][1] - sub0);
+          sc[j][2] = exp2f(sc[j][2] - sub1);
+          sc[j][3] = exp2f(sc[j][3] - sub1);
+          rs0 += sc[j][0] + sc[j][1];
+          rs1 += sc[j][2] + sc[j][3];
+        }
+        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+        lrow[sl][0] = lrow[sl][0] * a0 + rs0;
+        lrow[sl][1] = lrow[sl][1] * a1 + rs1;
+        mrow[sl][0] = nm0;
+        mrow[sl][1] = nm1;
+        uint32_t pa[4];
+        pa[0] = pack2(sc[0][0], sc[0][1]);
+        pa[1] = pack2(sc[0][2], sc[0][3]);
+        pa[2] = pack2(sc[1][0], sc[1][1]);
+        pa[3] = pack2(sc[1][2], sc[1][3]);
+#pragma unroll
+        for (int n = 0; n < HD / 16; ++n) {
+          o[sl][2 * n][0] *= a0;
+          o[sl][2 * n][1] *= a0;
+          o[sl][2 * n][2] *= a1;
+          o[sl][2 * n][3] *= a1;
+          o[sl][2 * n + 1][0] *= a0;
+          o[sl][2 * n + 1][1] *= a0;
+          o[sl][2 * n + 1][2] *= a1;
+          o[sl][2 * n + 1][3] *= a1;
+          uint32_t b0, b1, b2, b3;
+          const int key = warp * 16 + (lane & 15);
+          const int ch = n * 2 + (lane >> 4);
+          ldsm_x4_t(b0, b1, b2, b3, &V[swz<HD>(key, ch)]);
+          mma16816(o[sl][2 * n], pa, b0, b1);
+          mma16816(o[sl][2 * n + 1], pa, b2, b3);
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+
+  // ---- merge the 4 warps' partial states in warp order (smem reuses the K/V ring)
+  float* cO = reinterpret_cast<float*>(sm);                  // [4][ROWS][HD]
+  float* cM = cO + 4 * ROWS * HD;                            // [4][ROWS]
+  float* cL = cM + 4 * ROWS;                                 // [4][ROWS]
+#pragma unroll
+  for (int sl = 0; sl < SL; ++sl) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = sl * 16 + (lane >> 2) + 8 * h;
+      float* dst = cO + ((size_t)warp * ROWS + r) * HD;
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        const int col = i * 8 + 2 * (lane & 3);
+        dst[col] = o[sl][i][2 * h];
+        dst[col + 1] = o[sl][i][2 * h + 1];
+      }
+      if ((lane & 3) == 0) {
+        cM[warp * ROWS + r] = mrow[sl][h];
+        cL[warp * ROWS + r] = lrow[sl][h];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ROWS * (HD / 2); e += blockDim.x) {
+    const int r = e / (HD / 2), d = (e % (HD / 2)) * 2;
+    const int rr = tile * ROWS + r;
+    if (rr >= rows_total) continue;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) mx = fmaxf(mx, cM[w * ROWS + r]);
+    float num0 = 0.f, num1 = 0.f, den = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = cM[w * ROWS + r];
+      const float sc = mw == -INFINITY ? 0.f : exp2f(mw - mx);
+      den += cL[w * ROWS + r] * sc;
+      num0 += cO[((size_t)w * ROWS + r) * HD + d] * sc;
+      num1 += cO[((size_t)w * ROWS + r) * HD + d + 1] * sc;
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
+    *reinterpret_cast<uint32_t*>(dst) = pack2(num0 * inv, num1 * inv);
+  }
+}
+
+template <int HD, int SL>
+int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
+                 const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
+                 int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
+                 void* d_out, cudaStream_t st) {
+  constexpr int ROWS = 16 * SL;
+  const int ring = 2 * 3 * 64 * HD * 2;                  // K + V stages
+  const int merge = 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4;
+  const int smem = (ring > merge ? ring : merge) + ROWS * HD * 2;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_attention2<HD, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  const int G = H / KVH;
+  dim3 grid((max_q_len * G + ROWS - 1) / ROWS, KVH, n_seq);
+  k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
+                                                (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
+                                                d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                (__nv_bfloat16*)d_out);
+  return 0;
+}
+
 }  // namespace hm
 
 extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
@@ -259,7 +521,22 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
   dim3 grid((max_q_len * G + hm::AT_ROWS - 1) / hm::AT_ROWS, KVH, n_seq);
   const float scale_log2 = scale * 1.4426950408889634f;
   cudaStream_t st = (cudaStream_t)stream;
-  if (hd == 128) {
+  const bool v1 = getenv("HM_ATTN_V1") != nullptr;   // A/B switch for profiling only
+  if (!v1 && (hd == 128 || hd == 64)) {
+    // rows per CTA tile: 16 when a whole (sequence, kv head) block fits, else 32
+    const bool one = max_q_len * G <= 16;
+    if (hd == 128) {
+      if (one) hm::launch_attn2<128, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
+                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+      else hm::launch_attn2<128, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
+                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+    } else {
+      if (one) hm::launch_attn2<64, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
+                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+      else hm::launch_attn2<64, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
+                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+    }
+  } else if (hd == 128) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;
     static bool set = false;
     if (!set) { cudaFuncSetAttribute(hm::k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set = true; }

@@ -344,7 +344,7 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
 
 extern "C" int hm_gemm_bn(int32_t n) {
   // tile width is a function of N only (batch invariance): 256 when it divides N and N is wide
-  return (n % 256 == 0 && n >= 2048) ? 256 : 128;
+  return (n % 256 == 0 && n >= 1536) ? 256 : 128;
 }
 
 extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,

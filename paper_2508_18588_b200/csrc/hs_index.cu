@@ -284,16 +284,28 @@ __global__ void k_slot_stats(const int32_t* __restrict__ lcp, const int32_t* __r
                              const int32_t* __restrict__ rem, const uint8_t* __restrict__ node_flags,
                              SlotMap M, int64_t n, unsigned long long* __restrict__ counts) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  int32_t p = sa[k];
-  int32_t slot = M.resp_slot[M.rid[p]];
   unsigned long long c = 0;
-  int32_t v = lcp[k];
-  if (v < 0) c += 1;                                      // root
-  else if (v > 0 && (node_flags[k] & 3) == 3) c += 1;     // branching node
-  bool dup = v >= 0 && v == rem[p] && rem[sa[k - 1]] == v;
-  if (!dup) c += 1;                                       // distinct suffix leaf
-  atomicAdd(&counts[slot], c);
+  int32_t slot = -1;
+  if (k < n) {
+    int32_t p = sa[k];
+    slot = M.resp_slot[M.rid[p]];
+    int32_t v = lcp[k];
+    if (v < 0) c += 1;                                      // root
+    else if (v > 0 && (node_flags[k] & 3) == 3) c += 1;     // branching node
+    bool dup = v >= 0 && v == rem[p] && rem[sa[k - 1]] == v;
+    if (!dup) c += 1;                                       // distinct suffix leaf
+  }
+  // consecutive SA indices share a slot: add per (warp, slot) run, one atomic per run
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned same = __match_any_sync(0xffffffffu, slot);
+  const int leader = __ffs(same) - 1;
+  unsigned long long tot = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_down_sync(0xffffffffu, tot, o);
+    // only add lanes of the same run (runs are contiguous in lane order)
+    if (lane + o < 32 && ((same >> (lane + o)) & 1)) tot += y;
+  }
+  if ((int)lane == leader && slot >= 0) atomicAdd(&counts[slot], tot);
 }
 
 __global__ void k_count_groups(const int32_t* __restrict__ lcp, const int32_t* __restrict__ sa,
