@@ -360,20 +360,46 @@ def run_rollout(args, dist, pk):
     from paper_2508_18588_b200.model import PRESETS, Weights
     from paper_2508_18588_b200.model import lib as mlib
 
+    from paper_2508_18588_b200 import workers as W
+
     cfg = PRESETS[args.model]
     dev = torch.device("cuda", dist.local)
     torch.cuda.set_device(dev)
     B, S, P, T, G = args.batch, args.samples, args.prompt_len, args.length, 8
-    n_prompts = B // S
+    n_prompts = B // S                  # prompts per rank per wave
+    world, rank = dist.world, dist.rank
     w = Weights(cfg, dev, seed=args.seed)
+    bcast_ms = None
+    if world > 1:   # epoch boundary: the updated policy travels from rank 0 (NCCL over NVLink)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        W.broadcast_weights(w, src=0)
+        torch.cuda.synchronize()
+        bcast_ms = 1e3 * (time.perf_counter() - t0)
     eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev)
-    rng = np.random.default_rng([args.seed, 1000 + dist.rank])
-    prompts = np.repeat(rng.integers(0, cfg.vocab, size=(n_prompts, P), dtype=np.int32), S, axis=0)
-    # previous epoch: plain greedy rollout of the same engine (also the speculation-off baseline)
-    base = eng.rollout(prompts, [T] * B, speculate=False)
+
+    def prompt_tokens(pid):
+        return np.random.default_rng([args.seed, 1000 + pid]).integers(0, cfg.vocab, size=P, dtype=np.int32)
+
+    # HistoPipe assignment over last-epoch medians (uniform 4k rollouts here -> ranked by id)
+    medians = {pid: float(T) for pid in range(n_prompts * world)}
+    mine1 = W.assign_prompts(medians, world, 1)[rank]
+    prompts1 = np.repeat(np.stack([prompt_tokens(p) for p in mine1]), S, axis=0)
+    # previous epoch (step 1): plain greedy rollout of the same engine (also the speculation-off baseline)
+    base = eng.rollout(prompts1, [T] * B, speculate=False)
     nonspec_tps = B * T / (base.gpu_ms / 1e3)
-    truths = base.tokens[::S]
+    # epoch boundary: finished rollouts move to the rank owning the prompt at step 2 (all-to-all-v)
+    owner2 = W.owner_map(W.assign_prompts(medians, world, 2))
+    recv = W.route_rollouts([(pid, base.tokens[i * S], 1.0) for i, pid in enumerate(mine1)], owner2, rank, world,
+                            device=dev if world > 1 else "cpu")
+    recv.sort(key=lambda r: r[0])
+    mine2 = [r[0] for r in recv]
+    truths = np.stack([r[1] for r in recv])
+    rng = np.random.default_rng([args.seed, 2000 + rank])
     hist, rew = derived_history(rng, truths, args.similarity, G, cfg.vocab)
+    prompts = np.repeat(np.stack([prompt_tokens(p) for p in mine2]), S, axis=0)
+    expect = np.repeat(truths, S, axis=0)
+    owner3 = W.owner_map(W.assign_prompts(medians, world, 3))
     resp_off = np.arange(n_prompts * G + 1, dtype=np.int64) * T
     slot_resp_off = np.arange(n_prompts + 1, dtype=np.int64) * G
     reward_fx = (rew.reshape(-1) * float(1 << 32)).astype(np.int64)
@@ -382,7 +408,7 @@ def run_rollout(args, dist, pk):
     out_tok = torch.empty((B, T), dtype=torch.int32).pin_memory()
     slots = np.arange(B) // S
     stream = torch.cuda.current_stream(dev)
-    acc = {"ms": [], "res": None, "exact": True}
+    acc = {"ms": [], "res": None, "exact": True, "route_ms": []}
 
     def step():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -394,9 +420,14 @@ def run_rollout(args, dist, pk):
         e1.record(stream)
         out_tok.copy_(torch.from_numpy(res.tokens))   # results already read back by rollout(); keep pinned copy
         e1.synchronize()
+        # per-epoch history update: this step's rollouts go to their next owners
+        t0 = time.perf_counter()
+        W.route_rollouts([(pid, res.tokens[i * S], 1.0) for i, pid in enumerate(mine2)], owner3, rank, world,
+                         device=dev if world > 1 else "cpu")
+        acc["route_ms"].append(1e3 * (time.perf_counter() - t0))
         acc["ms"].append(e0.elapsed_time(e1))
         acc["res"] = res
-        acc["exact"] &= bool(np.array_equal(res.tokens, base.tokens))
+        acc["exact"] &= bool(np.array_equal(res.tokens, expect))
 
     lc0, mc0, gl0 = _lib.load().hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
     e2e_ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
@@ -459,7 +490,11 @@ def run_rollout(args, dist, pk):
         "engine_iterations": res.iterations,
         "nonspec_value": dist.sum(B * T) / dist.max(base.gpu_ms / 1e3),
         "speedup_vs_nonspec": value / max(nonspec_tps, 1e-9) if dist.world == 1 else None,
-        "bit_exact_vs_greedy": acc["exact"],
+        "bit_exact_vs_greedy": bool(dist.sum(float(acc["exact"])) == world),
+        "collectives": {"weight_broadcast_ms": bcast_ms, "rollout_route_ms_per_step": float(np.mean(
+            acc["route_ms"][-args.steps:])), "note": "epoch-boundary only: NCCL broadcast of the policy, "
+                                                     "all-to-all-v of finished rollouts to next-step owners "
+                                                     "(HistoPipe alternating assignment)"},
         "distinct_4gram_ratio": distinct,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(h_prompts.numel() * 4 + h_hist.numel() * 4),
                 "d2h_bytes_per_step": int(out_tok.numel() * 4 + B * 5 * 8)},

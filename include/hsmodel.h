@@ -32,6 +32,7 @@ extern "C" {
 #define HM_EPI_SWIGLU 1    /* out bf16 [M, N/2] = silu(gate) * up; W rows interleaved in hm_gemm_bn(N)/2 halves */
 #define HM_EPI_RESIDUAL 2  /* resid fp32 += acc */
 #define HM_EPI_ARGMAX 3    /* per 128-column tile (max, argmax) partials */
+#define HM_EPI_F32 4       /* out fp32 [M, ldr] = acc (residual add fused into hm_rmsnorm_residual) */
 
 typedef void* hm_stream_t;
 
@@ -57,6 +58,11 @@ int hm_embed(const int32_t* d_tokens, const void* d_emb, int32_t M, int32_t d, f
 /* out bf16 = x * rsqrt(mean(x^2) + eps) * w  (row-local, fixed reduction order) */
 int hm_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t d, float eps, void* d_out,
                const int32_t* d_m, hm_stream_t stream);
+
+/* x += y (both fp32 [M, d], y may be NULL), then out bf16 = rmsnorm(x) * w.
+ * Fuses the residual add of the previous O/down projection into the norm. */
+int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w, int32_t M, int32_t d, float eps, void* d_out,
+                        const int32_t* d_m, hm_stream_t stream);
 
 /* RoPE (rotate-half, table cos/sin [max_pos, hd/2] fp32) on q and k of the fused
  * qkv rows, q -> d_q [M, H, hd]; k, v -> cache[slot][kvh][pos][hd] */

@@ -16,7 +16,8 @@
 // Fused epilogues:
 //   EPI_STORE    bf16 out (+ bias)                         QKV (bias), generic
 //   EPI_SWIGLU   silu(gate) * up, W rows interleaved in BN/2 halves
-//   EPI_RESIDUAL fp32 residual += acc                      O-proj, down-proj
+//   EPI_RESIDUAL fp32 residual += acc (read-modify-write)
+//   EPI_F32      fp32 out = acc                            O-proj, down-proj (add fused into RMSNorm)
 //   EPI_ARGMAX   per-row (max, first argmax) partial per 128-column tile
 //
 // Batch invariance (bit-exact greedy under speculation): BN is a function of
@@ -39,7 +40,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle row
 constexpr int kThreads = 192;    // 6 warps
 
-enum { EPI_STORE = 0, EPI_SWIGLU = 1, EPI_RESIDUAL = 2, EPI_ARGMAX = 3 };
+enum { EPI_STORE = 0, EPI_SWIGLU = 1, EPI_RESIDUAL = 2, EPI_ARGMAX = 3, EPI_F32 = 4 };
 
 struct EpiParams {
   int M, N, K;
@@ -181,7 +182,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
       const uint32_t t_row = tmem + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
       const int row = m_blk * BM + q * 32 + lane;
       const bool live = row < M;
-      if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL) {
+      if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL || EPI == EPI_F32) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
@@ -194,6 +195,11 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
           if (live) {
             if constexpr (EPI == EPI_STORE) {
               store_bf16x32(p.out + (size_t)row * p.ldo + col0, v);
+            } else if constexpr (EPI == EPI_F32) {
+              // fire-and-forget fp32 store (the residual add is fused into the next RMSNorm)
+              float4* dst = reinterpret_cast<float4*>(p.resid + (size_t)row * p.ldr + col0);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             } else {
               float4* dst = reinterpret_cast<float4*>(p.resid + (size_t)row * p.ldr + col0);
 #pragma unroll
@@ -380,6 +386,7 @@ extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_
       case HM_EPI_STORE: return launch<256, 4, hm::EPI_STORE>(mx, mw, p, st);
       case HM_EPI_SWIGLU: return launch<256, 4, hm::EPI_SWIGLU>(mx, mw, p, st);
       case HM_EPI_RESIDUAL: return launch<256, 4, hm::EPI_RESIDUAL>(mx, mw, p, st);
+      case HM_EPI_F32: return launch<256, 4, hm::EPI_F32>(mx, mw, p, st);
       case HM_EPI_ARGMAX: return launch<256, 4, hm::EPI_ARGMAX>(mx, mw, p, st);
     }
   } else {
@@ -387,6 +394,7 @@ extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_
       case HM_EPI_STORE: return launch<128, 6, hm::EPI_STORE>(mx, mw, p, st);
       case HM_EPI_SWIGLU: return launch<128, 6, hm::EPI_SWIGLU>(mx, mw, p, st);
       case HM_EPI_RESIDUAL: return launch<128, 6, hm::EPI_RESIDUAL>(mx, mw, p, st);
+      case HM_EPI_F32: return launch<128, 6, hm::EPI_F32>(mx, mw, p, st);
       case HM_EPI_ARGMAX: return launch<128, 6, hm::EPI_ARGMAX>(mx, mw, p, st);
     }
   }

@@ -67,6 +67,54 @@ __global__ void k_rmsnorm(const float* __restrict__ x, const __nv_bfloat16* __re
   }
 }
 
+// x += y (fp32), out = rmsnorm(x) * w; warp per row, same fixed reduction order as k_rmsnorm
+__global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restrict__ y,
+                                   const __nv_bfloat16* __restrict__ w, int M, int d, float eps, const int* m_dev,
+                                   __nv_bfloat16* __restrict__ out) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int m = m_dev ? *m_dev : M;
+  if (row >= m) return;
+  float4* xr = reinterpret_cast<float4*>(x + (size_t)row * d);
+  const float4* yr = reinterpret_cast<const float4*>(y + (size_t)row * d);
+  constexpr int MAXV = 32;   // d <= 4096 keeps the row in registers (lane owns d/128 float4s)
+  float4 v[MAXV];
+  float ss = 0.f;
+  const int nv = d / 4;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      float4 a = xr[i];
+      const float4 b = yr[i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+      xr[i] = a;
+      v[k] = a;
+      ss += a.x * a.x;
+      ss += a.y * a.y;
+      ss += a.z * a.z;
+      ss += a.w * a.w;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = rsqrtf(ss / (float)d + eps);
+  __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * d);
+  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(w);
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      float2 wa = __bfloat1622float2(w2[2 * i]), wb = __bfloat1622float2(w2[2 * i + 1]);
+      orow[2 * i] = __floats2bfloat162_rn(v[k].x * r * wa.x, v[k].y * r * wa.y);
+      orow[2 * i + 1] = __floats2bfloat162_rn(v[k].z * r * wb.x, v[k].w * r * wb.y);
+    }
+  }
+}
+
 // one block per row: threads cover (H + KVH) * hd/2 rotations and KVH * hd/2 v pairs
 __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
                           const int32_t* __restrict__ row_slot, const float* __restrict__ cosb,
@@ -76,37 +124,47 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* 
   const int row = blockIdx.x;
   const int m = m_dev ? *m_dev : M;
   if (row >= m) return;
+  // 8 elements (16 B) per work item: rotations pair chunk i of the first half with chunk i of the second
   const int half = hd / 2;
+  const int hc = half / 8;                 // 16-byte chunks per half head
   const int p = pos[row];
   const int slot = row_slot[row];
   const __nv_bfloat16* src = qkv + (size_t)row * (H + 2 * KVH) * hd;
   const float* c = cosb + (size_t)p * half;
   const float* s = sinb + (size_t)p * half;
-  const int n_rot = (H + KVH) * half;
-  for (int t = threadIdx.x; t < n_rot + KVH * half; t += blockDim.x) {
+  const int n_rot = (H + KVH) * hc;
+  for (int t = threadIdx.x; t < n_rot + KVH * 2 * hc; t += blockDim.x) {
     if (t < n_rot) {
-      const int head = t / half, i = t % half;
+      const int head = t / hc, i = (t % hc) * 8;
       const __nv_bfloat16* hsrc = src + head * hd;
-      const float a = __bfloat162float(hsrc[i]), b = __bfloat162float(hsrc[i + half]);
-      const float ra = a * c[i] - b * s[i];
-      const float rb = b * c[i] + a * s[i];
-      if (head < H) {
-        __nv_bfloat16* dst = q + ((size_t)row * H + head) * hd;
-        dst[i] = __float2bfloat16_rn(ra);
-        dst[i + half] = __float2bfloat16_rn(rb);
-      } else {
-        const int kh = head - H;
-        __nv_bfloat16* dst = kc + (size_t)slot * slot_stride + ((size_t)kh * max_len + p) * hd;
-        dst[i] = __float2bfloat16_rn(ra);
-        dst[i + half] = __float2bfloat16_rn(rb);
+      const uint4 ua = *reinterpret_cast<const uint4*>(hsrc + i);
+      const uint4 ub = *reinterpret_cast<const uint4*>(hsrc + i + half);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&ua);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&ub);
+      const float4 c0 = *reinterpret_cast<const float4*>(c + i), c1 = *reinterpret_cast<const float4*>(c + i + 4);
+      const float4 s0 = *reinterpret_cast<const float4*>(s + i), s1 = *reinterpret_cast<const float4*>(s + i + 4);
+      const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      uint4 ra, rb;
+      __nv_bfloat162* ra2 = reinterpret_cast<__nv_bfloat162*>(&ra);
+      __nv_bfloat162* rb2 = reinterpret_cast<__nv_bfloat162*>(&rb);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 a = __bfloat1622float2(a2[e]), b = __bfloat1622float2(b2[e]);
+        ra2[e] = __floats2bfloat162_rn(a.x * cc[2 * e] - b.x * ss[2 * e], a.y * cc[2 * e + 1] - b.y * ss[2 * e + 1]);
+        rb2[e] = __floats2bfloat162_rn(b.x * cc[2 * e] + a.x * ss[2 * e], b.y * cc[2 * e + 1] + a.y * ss[2 * e + 1]);
       }
+      __nv_bfloat16* dst;
+      if (head < H) dst = q + ((size_t)row * H + head) * hd;
+      else dst = kc + (size_t)slot * slot_stride + ((size_t)(head - H) * max_len + p) * hd;
+      *reinterpret_cast<uint4*>(dst + i) = ra;
+      *reinterpret_cast<uint4*>(dst + i + half) = rb;
     } else {
       const int u = t - n_rot;
-      const int kh = u / half, i = (u % half) * 2;
+      const int kh = u / (2 * hc), i = (u % (2 * hc)) * 8;
       const __nv_bfloat16* vsrc = src + (H + KVH + kh) * hd;
       __nv_bfloat16* dst = vc + (size_t)slot * slot_stride + ((size_t)kh * max_len + p) * hd;
-      dst[i] = vsrc[i];
-      dst[i + 1] = vsrc[i + 1];
+      *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(vsrc + i);
     }
   }
 }
@@ -192,12 +250,25 @@ extern "C" int hm_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t 
   return HM_OK;
 }
 
+extern "C" int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w, int32_t M, int32_t d, float eps,
+                                   void* d_out, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (d % 4 || d > 4096) { hm_set_error("rmsnorm_residual: d % 4 == 0 and d <= 4096"); return HM_ERR_INVALID; }
+  if (!d_y) return hm_rmsnorm(d_x, d_w, M, d, eps, d_out, d_m, stream);
+  const int rows = 8;
+  hm::k_rmsnorm_residual<<<(M + rows - 1) / rows, 32 * rows, 0, (cudaStream_t)stream>>>(
+      d_x, d_y, (const __nv_bfloat16*)d_w, M, d, eps, d_m, (__nv_bfloat16*)d_out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
 extern "C" int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_row_slot,
                                  const float* d_cos, const float* d_sin, int32_t M, int32_t H, int32_t KVH,
                                  int32_t hd, void* d_q, void* d_kcache, void* d_vcache, int64_t slot_stride,
                                  int32_t max_len, const int32_t* d_m, hm_stream_t stream) {
   if (M <= 0) return HM_OK;
-  hm::k_rope_kv<<<M, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_qkv, d_pos, d_row_slot, d_cos, d_sin,
+  if (hd % 16) { hm_set_error("rope: head_dim % 16"); return HM_ERR_INVALID; }
+  hm::k_rope_kv<<<M, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_qkv, d_pos, d_row_slot, d_cos, d_sin,
                                                      M, H, KVH, hd, (__nv_bfloat16*)d_q, (__nv_bfloat16*)d_kcache,
                                                      (__nv_bfloat16*)d_vcache, slot_stride, max_len, d_m);
   HM_LAUNCH_CHECK();

@@ -34,11 +34,12 @@ SIGNATURES = {
     "hm_gemm_bn": [_I32],
     "hm_embed": [_P, _P, _I32, _I32, _P, _P, _P],
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
+    "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
     "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P],
     "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
-EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX = 0, 1, 2, 3
+EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX, EPI_F32 = 0, 1, 2, 3, 4
 
 _lib_model = None
 _lock = threading.Lock()
@@ -205,6 +206,7 @@ class Forward:
         M, d = max_rows, cfg.d_model
         bf = dict(dtype=torch.bfloat16, device=device)
         self.x = torch.empty((M, d), dtype=torch.float32, device=device)
+        self.y = torch.empty((M, d), dtype=torch.float32, device=device)   # O/down-proj output, added in the norm
         self.h = torch.empty((M, d), **bf)
         self.qkv = torch.empty((M, cfg.qkv_dim), **bf)
         self.q = torch.empty((M, cfg.n_heads, cfg.head_dim), **bf)
@@ -246,10 +248,13 @@ class Forward:
 
         k("embed", lambda: L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
         hd_all = cfg.n_heads * cfg.head_dim
+        y = self.y.data_ptr()
         for li, layer in enumerate(w.layers):
             kc, vc = self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr()
-            k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), layer["ln1"].data_ptr(), M, d, cfg.eps,
-                                              self.h.data_ptr(), mp, st))
+            # x += y (previous down-proj; none before layer 0), h = rmsnorm(x)
+            yp = None if li == 0 else y
+            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yp, layer["ln1"].data_ptr(), M, d,
+                                                       cfg.eps, self.h.data_ptr(), mp, st))
             k("gemm_qkv", lambda: L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M,
                                             cfg.qkv_dim, d, layer["bqkv"].data_ptr(), self.qkv.data_ptr(),
                                             cfg.qkv_dim, None, 0, None, None, mp, st))
@@ -262,18 +267,17 @@ class Forward:
                                                   kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
                                                   self.attn.data_ptr(), st))
-            k("gemm_o", lambda: L.hm_gemm(EPI_RESIDUAL, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
-                                          M, d, hd_all, None, None, 0, self.x.data_ptr(), d, None, None, mp, st))
-            k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), layer["ln2"].data_ptr(), M, d, cfg.eps,
-                                              self.h.data_ptr(), mp, st))
+            k("gemm_o", lambda: L.hm_gemm(EPI_F32, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
+                                          M, d, hd_all, None, None, 0, y, d, None, None, mp, st))
+            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, layer["ln2"].data_ptr(), M, d, cfg.eps,
+                                                       self.h.data_ptr(), mp, st))
             k("gemm_gate_up", lambda: L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M,
                                                 2 * cfg.ffn, d, None, self.act.data_ptr(), cfg.ffn, None, 0, None,
                                                 None, mp, st))
-            k("gemm_down", lambda: L.hm_gemm(EPI_RESIDUAL, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
-                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, self.x.data_ptr(), d, None, None,
-                                             mp, st))
-        k("rmsnorm", lambda: L.hm_rmsnorm(self.x.data_ptr(), w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(),
-                                          mp, st))
+            k("gemm_down", lambda: L.hm_gemm(EPI_F32, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
+                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y, d, None, None, mp, st))
+        k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, w.final_ln.data_ptr(), M, d, cfg.eps,
+                                                   self.h.data_ptr(), mp, st))
         if logits_out is not None:
             check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
                             logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))
