@@ -67,7 +67,9 @@ __global__ void k_rmsnorm(const float* __restrict__ x, const __nv_bfloat16* __re
   }
 }
 
-// x += y (fp32), out = rmsnorm(x) * w; warp per row, same fixed reduction order as k_rmsnorm
+// x += y (fp32), out = rmsnorm(x) * w; warp per row, same fixed reduction order as k_rmsnorm.
+// MAXV = ceil(d / 128) float4 per lane, so the row stays in registers.
+template <int MAXV>
 __global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restrict__ y,
                                    const __nv_bfloat16* __restrict__ w, int M, int d, float eps, const int* m_dev,
                                    __nv_bfloat16* __restrict__ out) {
@@ -77,7 +79,6 @@ __global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restric
   if (row >= m) return;
   float4* xr = reinterpret_cast<float4*>(x + (size_t)row * d);
   const float4* yr = reinterpret_cast<const float4*>(y + (size_t)row * d);
-  constexpr int MAXV = 32;   // d <= 4096 keeps the row in registers (lane owns d/128 float4s)
   float4 v[MAXV];
   float ss = 0.f;
   const int nv = d / 4;
@@ -256,8 +257,18 @@ extern "C" int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w
   if (d % 4 || d > 4096) { hm_set_error("rmsnorm_residual: d % 4 == 0 and d <= 4096"); return HM_ERR_INVALID; }
   if (!d_y) return hm_rmsnorm(d_x, d_w, M, d, eps, d_out, d_m, stream);
   const int rows = 8;
-  hm::k_rmsnorm_residual<<<(M + rows - 1) / rows, 32 * rows, 0, (cudaStream_t)stream>>>(
-      d_x, d_y, (const __nv_bfloat16*)d_w, M, d, eps, d_m, (__nv_bfloat16*)d_out);
+  const dim3 grid((M + rows - 1) / rows), block(32 * rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  const __nv_bfloat16* w = (const __nv_bfloat16*)d_w;
+  __nv_bfloat16* out = (__nv_bfloat16*)d_out;
+  const int nv = (d + 127) / 128;
+  if (nv <= 2) hm::k_rmsnorm_residual<2><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else if (nv <= 4) hm::k_rmsnorm_residual<4><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else if (nv <= 8) hm::k_rmsnorm_residual<8><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else if (nv <= 12) hm::k_rmsnorm_residual<12><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else if (nv <= 16) hm::k_rmsnorm_residual<16><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else if (nv <= 24) hm::k_rmsnorm_residual<24><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  else hm::k_rmsnorm_residual<32><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
   HM_LAUNCH_CHECK();
   return HM_OK;
 }
