@@ -102,14 +102,21 @@ class RolloutEngine:
         state.accept_greedy(first, q_off)
         return rows
 
-    def rollout(self, prompts, target_len, slots=None, index=None, speculate=True, record_tpi=False):
+    def rollout(self, prompts, target_len, slots=None, index=None, speculate=True, record_tpi=False,
+                recent_acceptance=None):
         """Generate target_len[b] tokens for each prompt row b (greedy), drafting from `index`.
 
         prompts: [B, P] int32 (host numpy or device tensor); slots[b]: history slot of b in index.
+        recent_acceptance: the worker's cumulative acceptance rate; when given, the batch gate
+        decides whether this batch speculates at all (spec_engine.gate_check, as sim.py:346-352).
         """
         import torch
+        from .spec_engine import gate_check
         prompts = torch.as_tensor(prompts, dtype=torch.int32).to(self.device)
         B, P = prompts.shape
+        if recent_acceptance is not None and not gate_check(self.spec.gate(), B, recent_acceptance):
+            speculate = False
+        self.last_speculated = bool(speculate and index is not None and self.spec.enabled)
         if B > self.n_slots:
             raise ValueError(f"batch {B} > engine slots {self.n_slots}")
         tl = np.asarray(target_len, dtype=np.int32)
