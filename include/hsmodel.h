@@ -44,6 +44,18 @@ int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t 
             int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
             float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream);
 
+/* Sampling LM head (rejection-sampling verify at temperature T): the argmax
+ * epilogue runs on logit/T + Gumbel(seed, key0[row], key1[row], v), a
+ * counter-based hash of (seed, sequence slot, position, token).  Gumbel-max is
+ * an exact sample of softmax(logit/T); verifying a point-mass draft x by
+ * "accept iff the row's sample == x" accepts with probability p(x) and, on
+ * rejection, emits a sample of p restricted to tokens != x -- the speculative
+ * sampling rule -- while keeping the output identical to non-speculative
+ * sampling with the same seed (bit-exact, batch-invariant). */
+int hm_lm_head_sample(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N, int32_t K,
+                      const int32_t* d_key0, const int32_t* d_key1, uint64_t seed, float temperature,
+                      float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream);
+
 /* GEMM tile width chosen for an N (a function of N only, never of M). */
 int hm_gemm_bn(int32_t n);
 

@@ -53,7 +53,30 @@ struct EpiParams {
   int* amax_idx;
   int n_amax_tiles;
   const int* m_dev;            // optional device-side M (CUDA-graph friendly)
+  // ARGMAX sampling mode (inv_temp > 0): per-row RNG keys (sequence slot, position)
+  const int* key0;
+  const int* key1;
+  unsigned long long seed;
+  float inv_temp;
 };
+
+// Counter-based hash RNG for Gumbel-max sampling: the noise of vocabulary entry v
+// at (seed, sequence, position) is a pure function of those four integers, so a
+// row samples the same token whatever else is in the batch.
+__device__ __forceinline__ uint64_t mix_u64(uint64_t x) {
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27; x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+__device__ __forceinline__ uint64_t gumbel_row_key(uint64_t seed, int k0, int k1) {
+  return mix_u64(seed ^ mix_u64(((uint64_t)(uint32_t)k0 << 32) | (uint32_t)k1));
+}
+__device__ __forceinline__ float gumbel(uint64_t rkey, int v) {
+  const uint32_t h = (uint32_t)(mix_u64(rkey + (uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ULL) >> 32);
+  const float u = ((float)h + 0.5f) * 2.3283064365386963e-10f;   // (0, 1)
+  return -__logf(-__logf(u));
+}
 
 template <int BN, int kStages>
 struct Cfg {
@@ -226,6 +249,10 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
           if (live) store_bf16x32(p.out + (size_t)row * p.ldo + n_blk * H + c, g);
         }
       } else {  // EPI_ARGMAX: one partial per 128 columns
+        // sampling (inv_temp > 0): Gumbel-max over logit/T + g(seed, key0[row], key1[row], col)
+        const bool sample = p.inv_temp > 0.f && live;
+        uint64_t rkey = 0;
+        if (sample) rkey = gumbel_row_key(p.seed, p.key0[row], p.key1[row]);
 #pragma unroll 1
         for (int h = 0; h < BN; h += 128) {
           float best = -INFINITY;
@@ -234,6 +261,10 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
           for (int c = h; c < h + 128; c += 32) {
             float v[32];
             tmem_ld32(t_row + c, v);
+            if (sample) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = v[i] * p.inv_temp + gumbel(rkey, n_blk * BN + c + i);
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (v[i] > best) { best = v[i]; bidx = n_blk * BN + c + i; }   // strict: first max wins
@@ -353,9 +384,34 @@ extern "C" int hm_gemm_bn(int32_t n) {
   return (n % 256 == 0 && n >= 1536) ? 256 : 128;
 }
 
+static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
+                     int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
+                     float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, const int32_t* key0,
+                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream);
+
 extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
                        int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
                        float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, hm_stream_t stream) {
+  return gemm_impl(epi, d_x, ldx, d_w, ldw, M, N, K, d_bias, d_out, ldo, d_resid, ldr, d_amax_val, d_amax_idx, d_m,
+                   nullptr, nullptr, 0, 0.f, stream);
+}
+
+extern "C" int hm_lm_head_sample(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
+                                 int32_t K, const int32_t* d_key0, const int32_t* d_key1, uint64_t seed,
+                                 float temperature, float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m,
+                                 hm_stream_t stream) {
+  if (!(temperature > 0.f)) {
+    hm_set_error("hm_lm_head_sample: temperature must be > 0 (use HM_EPI_ARGMAX for greedy)");
+    return HM_ERR_INVALID;
+  }
+  return gemm_impl(HM_EPI_ARGMAX, d_x, ldx, d_w, ldw, M, N, K, nullptr, nullptr, 0, nullptr, 0, d_amax_val,
+                   d_amax_idx, d_m, d_key0, d_key1, seed, 1.f / temperature, stream);
+}
+
+static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
+                     int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
+                     float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, const int32_t* key0,
+                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream) {
   if (M <= 0) return HM_OK;
   if (K % hm::BK != 0 || N % 128 != 0) {
     hm_set_error("hm_gemm: K must be a multiple of 64 and N of 128");
@@ -380,6 +436,10 @@ extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_
   p.amax_idx = d_amax_idx;
   p.n_amax_tiles = N / 128;
   p.m_dev = d_m;
+  p.key0 = key0;
+  p.key1 = key1;
+  p.seed = seed;
+  p.inv_temp = inv_temp;
   cudaStream_t st = (cudaStream_t)stream;
   if (BN == 256) {
     switch (epi) {

@@ -51,7 +51,7 @@ class RolloutResult:
 class RolloutEngine:
     def __init__(self, cfg: ModelConfig, weights: Weights, n_slots: int, max_len: int, device,
                  spec: SpecConfig | None = None, prefill_rows: int = 16384, use_graphs: bool = True,
-                 check_every: int = 8):
+                 check_every: int = 8, temperature: float = 0.0, seed: int = 0):
         import torch
         self.use_graphs, self.check_every = use_graphs, check_every
         self.graph_launches = 0   # kernels executed by graph replays (not seen by the C launch counters)
@@ -61,6 +61,10 @@ class RolloutEngine:
         self.cache = KVCache(cfg, n_slots, max_len + self.spec.window_max + 2, self.device)
         self.max_q = 1 + self.spec.window_max
         self.fwd = Forward(weights, self.cache, max(prefill_rows, n_slots * self.max_q), self.device)
+        # T = 0: greedy verify (argmax); T > 0: rejection-sampling verify by Gumbel-max coupling --
+        # accept a point-mass draft x iff the row's sample equals x (probability p(x)), else emit the
+        # sample, which is then distributed as p restricted to tokens != x (hm_lm_head_sample)
+        self.fwd.temperature, self.fwd.seed = float(temperature), int(seed)
         self.prefill_rows = prefill_rows
         i32 = dict(dtype=torch.int32, device=self.device)
         R = self.fwd.max_rows

@@ -32,6 +32,7 @@ SIGNATURES = {
     "hm_gemm": [_I32, _P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _P, _I64, _P, _P, _P, _P],
     "hm_argmax_reduce": [_P, _P, _I32, _I32, _P, _P, _P],
     "hm_gemm_bn": [_I32],
+    "hm_lm_head_sample": [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, ctypes.c_uint64, _F32, _P, _P, _P, _P],
     "hm_embed": [_P, _P, _I32, _I32, _P, _P, _P],
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
@@ -218,6 +219,8 @@ class Forward:
         self.argmax = torch.empty(M, dtype=torch.int32, device=device)
         self.cos, self.sin = w.rope_tables(cache.max_len + 64, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
+        self.temperature = 0.0   # 0 = greedy argmax; > 0 = Gumbel-max sampling (hm_lm_head_sample)
+        self.seed = 0
 
     def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
             logits_out=None, prof=None):
@@ -281,9 +284,15 @@ class Forward:
         if logits_out is not None:
             check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
                             logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))
-        k("gemm_lm_head_argmax", lambda: L.hm_gemm(EPI_ARGMAX, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M,
-                                                   cfg.vocab, d, None, None, 0, None, 0, self.amax_val.data_ptr(),
-                                                   self.amax_idx.data_ptr(), mp, st))
+        if self.temperature > 0.0:
+            # rejection-sampling verify: Gumbel-max sample keyed by (seed, kv slot, position)
+            k("gemm_lm_head_argmax", lambda: L.hm_lm_head_sample(
+                self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, row_slot.data_ptr(), pos.data_ptr(),
+                self.seed, self.temperature, self.amax_val.data_ptr(), self.amax_idx.data_ptr(), mp, st))
+        else:
+            k("gemm_lm_head_argmax", lambda: L.hm_gemm(EPI_ARGMAX, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M,
+                                                       cfg.vocab, d, None, None, 0, None, 0,
+                                                       self.amax_val.data_ptr(), self.amax_idx.data_ptr(), mp, st))
         k("argmax_reduce", lambda: L.hm_argmax_reduce(self.amax_val.data_ptr(), self.amax_idx.data_ptr(), M,
                                                       self.n_tiles, mp, self.argmax.data_ptr(), st))
         return self.argmax[:M]
