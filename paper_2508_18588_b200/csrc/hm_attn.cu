@@ -272,11 +272,13 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   constexpr int ROWS = 16 * SL;
   constexpr int KS = 64;            // keys per stage (4 warps x 16)
   constexpr int NST = 3;            // pipeline stages
-  const int tile = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+  // one CTA per (kv head, sequence); it walks the sequence's row tiles (most verify blocks are one tile),
+  // so no CTA of a launch sized for the longest possible block is ever empty
+  const int kvh = blockIdx.x, s = blockIdx.y;
   const int G = H / KVH;
   const int ql = q_len[s];
   const int rows_total = ql * G;
-  if (tile * ROWS >= rows_total) return;
+  for (int tile = 0; tile * ROWS < rows_total; ++tile) {
   const int qo = q_off[s], p0 = pos0[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -484,6 +486,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
     *reinterpret_cast<uint32_t*>(dst) = pack2(num0 * inv, num1 * inv);
   }
+  __syncthreads();   // the next tile reuses the smem ring / merge buffers
+  }
 }
 
 template <int HD, int SL>
@@ -501,7 +505,8 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
     set = true;
   }
   const int G = H / KVH;
-  dim3 grid((max_q_len * G + ROWS - 1) / ROWS, KVH, n_seq);
+  (void)G;
+  dim3 grid(KVH, n_seq);
   k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                 (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
                                                 d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,

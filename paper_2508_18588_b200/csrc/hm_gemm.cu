@@ -292,10 +292,9 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
 // final argmax over the per-tile partials (tiles in column order; ties -> smallest index)
 __global__ void k_argmax_reduce(const float* __restrict__ val, const int* __restrict__ idx, int M, int n_tiles,
                                 const int* m_dev, int* __restrict__ out) {
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int m = m_dev ? *m_dev : M;
-  if (row >= m) return;
+  for (int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); row < m; row += gridDim.x * (blockDim.x / 32)) {
   float best = -INFINITY;
   int bi = 0x7fffffff;
   for (int t = lane; t < n_tiles; t += 32) {
@@ -309,6 +308,7 @@ __global__ void k_argmax_reduce(const float* __restrict__ val, const int* __rest
     if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
   }
   if (lane == 0) out[row] = bi;
+  }
 }
 
 }  // namespace hm
@@ -467,7 +467,8 @@ extern "C" int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_
   if (M <= 0) return HM_OK;
   int rows_per_block = 8;
   hm_count_launches(1);
-  hm::k_argmax_reduce<<<(M + rows_per_block - 1) / rows_per_block, 256, 0, (cudaStream_t)stream>>>(
+  const int blocks = (M + rows_per_block - 1) / rows_per_block;
+  hm::k_argmax_reduce<<<blocks < 1184 ? blocks : 1184, 256, 0, (cudaStream_t)stream>>>(
       d_val, d_idx, M, n_tiles, d_m, d_out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

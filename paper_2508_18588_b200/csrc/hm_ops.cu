@@ -30,21 +30,21 @@ namespace hm {
 
 __global__ void k_embed(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb, int M, int d,
                         const int* m_dev, float* __restrict__ x) {
-  const int row = blockIdx.x;
   const int m = m_dev ? *m_dev : M;
-  if (row >= m) return;
-  const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(emb + (size_t)tok[row] * d);
-  float2* dst = reinterpret_cast<float2*>(x + (size_t)row * d);
-  for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+  for (int row = blockIdx.x; row < m; row += gridDim.x) {   // grid-stride: launches sized for max rows stay cheap
+    const __nv_bfloat162* src = reinterpret_cast<const __nv_bfloat162*>(emb + (size_t)tok[row] * d);
+    float2* dst = reinterpret_cast<float2*>(x + (size_t)row * d);
+    for (int i = threadIdx.x; i < d / 2; i += blockDim.x) dst[i] = __bfloat1622float2(src[i]);
+  }
 }
 
 // warp per row; each lane owns a fixed strided set of columns
 __global__ void k_rmsnorm(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int M, int d, float eps,
                           const int* m_dev, __nv_bfloat16* __restrict__ out) {
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int m = m_dev ? *m_dev : M;
-  if (row >= m) return;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m;
+       row += gridDim.x * (blockDim.x >> 5)) {
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
   float ss = 0.f;
   for (int i = lane; i < d / 4; i += 32) {
@@ -65,6 +65,7 @@ __global__ void k_rmsnorm(const float* __restrict__ x, const __nv_bfloat16* __re
     orow[2 * i] = __floats2bfloat162_rn(v.x * r * wa.x, v.y * r * wa.y);
     orow[2 * i + 1] = __floats2bfloat162_rn(v.z * r * wb.x, v.w * r * wb.y);
   }
+  }
 }
 
 // x += y (fp32), out = rmsnorm(x) * w; warp per row, same fixed reduction order as k_rmsnorm.
@@ -73,10 +74,10 @@ template <int MAXV>
 __global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restrict__ y,
                                    const __nv_bfloat16* __restrict__ w, int M, int d, float eps, const int* m_dev,
                                    __nv_bfloat16* __restrict__ out) {
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int m = m_dev ? *m_dev : M;
-  if (row >= m) return;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m;
+       row += gridDim.x * (blockDim.x >> 5)) {
   float4* xr = reinterpret_cast<float4*>(x + (size_t)row * d);
   const float4* yr = reinterpret_cast<const float4*>(y + (size_t)row * d);
   float4 v[MAXV];
@@ -114,17 +115,17 @@ __global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restric
       orow[2 * i + 1] = __floats2bfloat162_rn(v[k].z * r * wb.x, v[k].w * r * wb.y);
     }
   }
+  }
 }
 
-// one block per row: threads cover (H + KVH) * hd/2 rotations and KVH * hd/2 v pairs
+// block per row (grid-stride): threads cover the 16-byte chunks of q/k rotations and v copies
 __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
                           const int32_t* __restrict__ row_slot, const float* __restrict__ cosb,
                           const float* __restrict__ sinb, int M, int H, int KVH, int hd,
                           __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                           int64_t slot_stride, int max_len, const int* m_dev) {
-  const int row = blockIdx.x;
   const int m = m_dev ? *m_dev : M;
-  if (row >= m) return;
+  for (int row = blockIdx.x; row < m; row += gridDim.x) {
   // 8 elements (16 B) per work item: rotations pair chunk i of the first half with chunk i of the second
   const int half = hd / 2;
   const int hc = half / 8;                 // 16-byte chunks per half head
@@ -167,6 +168,7 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* 
       __nv_bfloat16* dst = vc + (size_t)slot * slot_stride + ((size_t)kh * max_len + p) * hd;
       *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(vsrc + i);
     }
+  }
   }
 }
 
@@ -235,7 +237,7 @@ __global__ void k_build_verify(int n_seq, const int32_t* __restrict__ gen_tok, i
 extern "C" int hm_embed(const int32_t* d_tokens, const void* d_emb, int32_t M, int32_t d, float* d_x,
                         const int32_t* d_m, hm_stream_t stream) {
   if (M <= 0) return HM_OK;
-  hm::k_embed<<<M, 128, 0, (cudaStream_t)stream>>>(d_tokens, (const __nv_bfloat16*)d_emb, M, d, d_m, d_x);
+  hm::k_embed<<<M < 2368 ? M : 2368, 128, 0, (cudaStream_t)stream>>>(d_tokens, (const __nv_bfloat16*)d_emb, M, d, d_m, d_x);
   HM_LAUNCH_CHECK();
   return HM_OK;
 }
@@ -245,7 +247,7 @@ extern "C" int hm_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t 
   if (M <= 0) return HM_OK;
   if (d % 4) { hm_set_error("rmsnorm: d % 4"); return HM_ERR_INVALID; }
   const int rows = 8;
-  hm::k_rmsnorm<<<(M + rows - 1) / rows, 32 * rows, 0, (cudaStream_t)stream>>>(
+  hm::k_rmsnorm<<<(M + rows - 1) / rows < 1184 ? (M + rows - 1) / rows : 1184, 32 * rows, 0, (cudaStream_t)stream>>>(
       d_x, (const __nv_bfloat16*)d_w, M, d, eps, d_m, (__nv_bfloat16*)d_out);
   HM_LAUNCH_CHECK();
   return HM_OK;
@@ -257,7 +259,7 @@ extern "C" int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w
   if (d % 4 || d > 4096) { hm_set_error("rmsnorm_residual: d % 4 == 0 and d <= 4096"); return HM_ERR_INVALID; }
   if (!d_y) return hm_rmsnorm(d_x, d_w, M, d, eps, d_out, d_m, stream);
   const int rows = 8;
-  const dim3 grid((M + rows - 1) / rows), block(32 * rows);
+  const dim3 grid((M + rows - 1) / rows < 1184 ? (M + rows - 1) / rows : 1184), block(32 * rows);
   cudaStream_t st = (cudaStream_t)stream;
   const __nv_bfloat16* w = (const __nv_bfloat16*)d_w;
   __nv_bfloat16* out = (__nv_bfloat16*)d_out;
@@ -279,7 +281,7 @@ extern "C" int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const 
                                  int32_t max_len, const int32_t* d_m, hm_stream_t stream) {
   if (M <= 0) return HM_OK;
   if (hd % 16) { hm_set_error("rope: head_dim % 16"); return HM_ERR_INVALID; }
-  hm::k_rope_kv<<<M, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_qkv, d_pos, d_row_slot, d_cos, d_sin,
+  hm::k_rope_kv<<<M < 2368 ? M : 2368, 128, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)d_qkv, d_pos, d_row_slot, d_cos, d_sin,
                                                      M, H, KVH, hd, (__nv_bfloat16*)d_q, (__nv_bfloat16*)d_kcache,
                                                      (__nv_bfloat16*)d_vcache, slot_stride, max_len, d_m);
   HM_LAUNCH_CHECK();

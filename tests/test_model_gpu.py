@@ -193,6 +193,69 @@ def test_tiny_engine_spec_equals_greedy_and_reference_replay(torch):
     assert spec.iterations < base.iterations
 
 
+def test_gumbel_sampling_marginal_matches_softmax(torch):
+    """hm_lm_head_sample draws from softmax(logit / T): chi-square over 100k keyed draws."""
+    import paper_2508_18588_b200.model as Mo
+    g = torch.Generator(device="cuda").manual_seed(9)
+    K, V, n = 64, 256, 100000
+    x1 = torch.randn(1, K, device="cuda", generator=g).to(torch.bfloat16)
+    x = x1.repeat(n, 1).contiguous()
+    E = (torch.randn(V, K, device="cuda", generator=g) * 0.3).to(torch.bfloat16)
+    T = 1.0
+    key0 = torch.arange(n, dtype=torch.int32, device="cuda")
+    key1 = torch.full((n,), 17, dtype=torch.int32, device="cuda")
+    nt = V // 128
+    av = torch.empty(n, nt, device="cuda")
+    ai = torch.empty(n, nt, dtype=torch.int32, device="cuda")
+    L = Mo.lib()
+    Mo.check(L.hm_lm_head_sample(x.data_ptr(), K, E.data_ptr(), K, n, V, K, key0.data_ptr(), key1.data_ptr(), 1234,
+                                 T, av.data_ptr(), ai.data_ptr(), None, 0))
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    Mo.check(L.hm_argmax_reduce(av.data_ptr(), ai.data_ptr(), n, nt, None, out.data_ptr(), 0))
+    counts = torch.bincount(out.long(), minlength=V).double().cpu()
+    p = torch.softmax((x1.float() @ E.float().T)[0] / T, 0).double().cpu()
+    exp = p * n
+    keep = exp >= 5
+    chi2 = float((((counts - exp) ** 2) / exp)[keep].sum())
+    dof = int(keep.sum()) - 1
+    assert chi2 < dof + 6 * (2 * dof) ** 0.5, (chi2, dof)
+    # same keys -> same draws (seeded, independent of batch composition)
+    sub = slice(1000, 1100)
+    av2, ai2 = av[:100].clone(), ai[:100].clone()
+    Mo.check(L.hm_lm_head_sample(x[sub].contiguous().data_ptr(), K, E.data_ptr(), K, 100, V, K,
+                                 key0[sub].contiguous().data_ptr(), key1[sub].contiguous().data_ptr(), 1234, T,
+                                 av2.data_ptr(), ai2.data_ptr(), None, 0))
+    out2 = torch.empty(100, dtype=torch.int32, device="cuda")
+    Mo.check(L.hm_argmax_reduce(av2.data_ptr(), ai2.data_ptr(), 100, nt, None, out2.data_ptr(), 0))
+    assert torch.equal(out2, out[sub])
+
+
+def test_tiny_engine_rejection_sampling_spec_equals_plain_sampling(torch):
+    """T = 1.0: HistoSpec output == plain sampling output with the same seed (Gumbel-max coupling),
+    and the accept profile == reference state machine on that output."""
+    from oracle import hs_oracle_c as C
+    from paper_2508_18588_b200.engine import RolloutEngine
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import TINY, Weights
+    from paper_2508_18588_b200.synth import mutate
+    w = Weights(TINY, "cuda", seed=3)
+    B, P, T = 16, 24, 160
+    eng = RolloutEngine(TINY, w, n_slots=B, max_len=P + T + 8, device="cuda", temperature=1.0, seed=99)
+    rng = np.random.default_rng(3)
+    prompts = rng.integers(0, TINY.vocab, size=(B, P), dtype=np.int32)
+    base = eng.rollout(prompts, [T] * B, speculate=False)
+    hist = [[(mutate(rng, base.tokens[b].astype(np.int64), 0.7, T, TINY.vocab, 4.0), 1.0) for _ in range(8)]
+            for b in range(B)]
+    spec = eng.rollout(prompts, [T] * B, slots=np.arange(B), index=GpuIndex(hist), speculate=True, record_tpi=True)
+    assert np.array_equal(spec.tokens, base.tokens)
+    per, _ = C.replay_batch(hist, [base.tokens[b] for b in range(B)], list(range(B)))
+    assert spec.tokens_per_iter == per
+    # sampling is not greedy: outputs differ from the T=0 engine
+    greedy = RolloutEngine(TINY, w, n_slots=B, max_len=P + T + 8, device="cuda").rollout(prompts, [T] * B,
+                                                                                        speculate=False)
+    assert not np.array_equal(greedy.tokens, base.tokens)
+
+
 def test_qwen_shape_engine_spec_equals_greedy(torch):
     """Qwen2.5-1.5B shape, small batch: bit-exact spec == greedy, profile == reference replay."""
     from oracle import hs_oracle_c as C
