@@ -122,7 +122,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = p.m_dev ? *p.m_dev : p.M;
   const int m_tiles = (M + BM - 1) / BM;
-  const int n_tiles = p.N / BN;
+  const int n_tiles = (p.N + BN - 1) / BN;
   const int total = m_tiles * n_tiles;
   if ((int)blockIdx.x >= total) return;   // uniform across the CTA
   const int num_k = p.K / BK;
@@ -205,9 +205,11 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
       const uint32_t t_row = tmem + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
       const int row = m_blk * BM + q * 32 + lane;
       const bool live = row < M;
+      // a last N tile may be half empty (N % 128 == 0, BN = 256): W rows past N were zero-filled by TMA
+      const int cmax = min(BN, p.N - n_blk * BN);
       if constexpr (EPI == EPI_STORE || EPI == EPI_RESIDUAL || EPI == EPI_F32) {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < cmax; c += 32) {
           float v[32];
           tmem_ld32(t_row + c, v);
           const int col0 = n_blk * BN + c;
@@ -254,7 +256,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
         uint64_t rkey = 0;
         if (sample) rkey = gumbel_row_key(p.seed, p.key0[row], p.key1[row]);
 #pragma unroll 1
-        for (int h = 0; h < BN; h += 128) {
+        for (int h = 0; h < cmax; h += 128) {
           float best = -INFINITY;
           int bidx = 0;
 #pragma unroll 1
@@ -365,7 +367,7 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int tiles = ((p.M + hm::BM - 1) / hm::BM) * (p.N / BN);
+  const int tiles = ((p.M + hm::BM - 1) / hm::BM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   hm_count_launches(1);
   kern<<<grid, hm::kThreads, C::kSmemBytes, st>>>(mx, mw, p);
@@ -380,8 +382,9 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
 }  // namespace
 
 extern "C" int hm_gemm_bn(int32_t n) {
-  // tile width is a function of N only (batch invariance): 256 when it divides N and N is wide
-  return (n % 256 == 0 && n >= 1536) ? 256 : 128;
+  // tile width is a function of N only (batch invariance): 256 for wide N (a last tile may be half
+  // empty when N % 256 == 128, e.g. the 151,936-entry LM head), 128 otherwise
+  return (n >= 1536) ? 256 : 128;
 }
 
 static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
@@ -418,6 +421,10 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
     return HM_ERR_INVALID;
   }
   const int BN = hm_gemm_bn(N);
+  if (epi == HM_EPI_SWIGLU && N % BN != 0) {
+    hm_set_error("hm_gemm: SwiGLU needs N to be a multiple of the tile width (interleave granularity)");
+    return HM_ERR_INVALID;
+  }
   CUtensorMap mx, mw;
   if (!make_map(&mx, d_x, M, K, ldx, hm::BM) || !make_map(&mw, d_w, N, K, ldw, BN)) {
     hm_set_error("cuTensorMapEncodeTiled failed (alignment: base 16 B, ld multiple of 8 elements)");

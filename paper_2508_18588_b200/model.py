@@ -112,7 +112,7 @@ PRESETS = {c.name: c for c in (TINY, QWEN25_1P5B, QWEN25_7B)}
 
 def gemm_bn(n: int) -> int:
     """Mirror of hm_gemm_bn: GEMM tile width for an output width n (function of n only)."""
-    return 256 if (n % 256 == 0 and n >= 1536) else 128
+    return 256 if n >= 1536 else 128
 
 
 def swiglu_half(ffn: int) -> int:

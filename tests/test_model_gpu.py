@@ -33,7 +33,7 @@ def _gemm(M_, epi, x, w, bias=None, out=None, resid=None, amax=None):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (1, 256, 128), (300, 384, 1536), (1000, 2048, 1536),
-                                   (77, 1536, 8960)])
+                                   (77, 1536, 8960), (200, 1664, 256)])   # 1664: half-empty last 256-wide tile
 def test_gemm_store_bias(torch, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
@@ -81,20 +81,20 @@ def test_gemm_swiglu_residual_argmax(torch):
     _gemm(M, 2, act, wd, resid=res)
     ref2 = res0 + act.float() @ wd.float().T
     assert torch.allclose(res, ref2, rtol=1e-4, atol=1e-3)
-    # argmax epilogue over a 4096-vocab head
-    V = 4096
-    E = (torch.randn(V, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
-    nt = V // 128
-    av = torch.empty(M, nt, device="cuda")
-    ai = torch.empty(M, nt, dtype=torch.int32, device="cuda")
-    _gemm(M, 3, x, E, amax=(av, ai))
+    # argmax epilogue over a 4096-vocab head and a head whose last 256-wide tile is half empty
     import paper_2508_18588_b200.model as Mo
-    out = torch.empty(M, dtype=torch.int32, device="cuda")
-    Mo.check(Mo.lib().hm_argmax_reduce(av.data_ptr(), ai.data_ptr(), M, nt, None, out.data_ptr(), 0))
-    logits = x.float() @ E.float().T
-    top2 = logits.topk(2, dim=1).values
-    sure = (top2[:, 0] - top2[:, 1]) > 1e-3
-    assert (out.long()[sure] == logits.argmax(1)[sure]).all()
+    for V in (4096, 1664):
+        E = (torch.randn(V, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+        nt = V // 128
+        av = torch.empty(M, nt, device="cuda")
+        ai = torch.empty(M, nt, dtype=torch.int32, device="cuda")
+        _gemm(M, 3, x, E, amax=(av, ai))
+        out = torch.empty(M, dtype=torch.int32, device="cuda")
+        Mo.check(Mo.lib().hm_argmax_reduce(av.data_ptr(), ai.data_ptr(), M, nt, None, out.data_ptr(), 0))
+        logits = x.float() @ E.float().T
+        top2 = logits.topk(2, dim=1).values
+        sure = (top2[:, 0] - top2[:, 1]) > 1e-3
+        assert (out.long()[sure] == logits.argmax(1)[sure]).all()
 
 
 def _attn_ref(torch, q, kc, vc, seqs, H, KVH, hd):
@@ -254,6 +254,30 @@ def test_tiny_engine_rejection_sampling_spec_equals_plain_sampling(torch):
     greedy = RolloutEngine(TINY, w, n_slots=B, max_len=P + T + 8, device="cuda").rollout(prompts, [T] * B,
                                                                                         speculate=False)
     assert not np.array_equal(greedy.tokens, base.tokens)
+
+
+def test_qwen7b_shape_rejection_sampling(torch):
+    """configs[2]: Qwen2.5-7B shape (untied head, GQA 7, V=152,064) at T=1.0, small batch:
+    speculative sampling output == plain sampling output; profile == reference replay."""
+    from oracle import hs_oracle_c as C
+    from paper_2508_18588_b200.engine import RolloutEngine
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import QWEN25_7B, Weights
+    from paper_2508_18588_b200.synth import mutate
+    w = Weights(QWEN25_7B, "cuda", seed=0)
+    B, P, T = 4, 48, 96
+    eng = RolloutEngine(QWEN25_7B, w, n_slots=B, max_len=P + T + 8, device="cuda", temperature=1.0, seed=5)
+    rng = np.random.default_rng(4)
+    prompts = rng.integers(0, QWEN25_7B.vocab, size=(B, P), dtype=np.int32)
+    base = eng.rollout(prompts, [T] * B, speculate=False)
+    hist = [[(mutate(rng, base.tokens[b].astype(np.int64), 0.7, T, QWEN25_7B.vocab, 4.0), 1.0) for _ in range(8)]
+            for b in range(B)]
+    spec = eng.rollout(prompts, [T] * B, slots=np.arange(B), index=GpuIndex(hist), speculate=True, record_tpi=True)
+    assert np.array_equal(spec.tokens, base.tokens)
+    per, _ = C.replay_batch(hist, [base.tokens[b] for b in range(B)], list(range(B)))
+    assert spec.tokens_per_iter == per
+    del eng, w
+    torch.cuda.empty_cache()
 
 
 def test_qwen_shape_engine_spec_equals_greedy(torch):
