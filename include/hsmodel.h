@@ -88,7 +88,8 @@ int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_
 int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t hd, int32_t max_len,
-                 float scale, void* d_out, hm_stream_t stream);
+                 float scale, void* d_out, int32_t* d_work /* [n_seq+1] scratch or NULL */,
+                 hm_stream_t stream);
 
 /* Verify-batch assembly for the rollout step: for each live sequence s
  * (gen_len < target_len) rows [last generated token, draft_1..draft_k] at

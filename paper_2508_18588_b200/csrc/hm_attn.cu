@@ -267,25 +267,23 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
                                                     const int32_t* __restrict__ pos0,
                                                     const int32_t* __restrict__ kv_slot, int H, int KVH,
                                                     int max_len, float scale_log2,
-                                                    __nv_bfloat16* __restrict__ out) {
+                                                    __nv_bfloat16* __restrict__ out, int n_seq,
+                                                    const int32_t* __restrict__ work) {
   constexpr int CH = HD / 8;        // 16-byte chunks per row
   constexpr int ROWS = 16 * SL;
   constexpr int KS = 64;            // keys per stage (4 warps x 16)
   constexpr int NST = 3;            // pipeline stages
-  // one CTA per (kv head, sequence); it walks the sequence's row tiles (most verify blocks are one tile),
-  // so no CTA of a launch sized for the longest possible block is ever empty
-  const int kvh = blockIdx.x, s = blockIdx.y;
   const int G = H / KVH;
-  const int ql = q_len[s];
-  const int rows_total = ql * G;
-  for (int tile = 0; tile * ROWS < rows_total; ++tile) {
-  const int qo = q_off[s], p0 = pos0[s];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
   extern __shared__ __align__(128) uint8_t sm[];
   uint4* sK = reinterpret_cast<uint4*>(sm);            // [NST][KS][CH]
   uint4* sV = sK + NST * KS * CH;                        // [NST][KS][CH]
   uint4* sQ = sV + NST * KS * CH;                        // [ROWS][CH]
+
+  // one work item = (sequence, row tile, kv head)
+  auto do_tile = [&](const int s, const int kvh, const int tile) {
+  const int rows_total = q_len[s] * G;
+  const int qo = q_off[s], p0 = pos0[s];
 
   for (int c = threadIdx.x; c < ROWS * CH; c += blockDim.x) {
     const int r = c / CH, ch = c % CH;
@@ -315,16 +313,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     }
   };
   __syncthreads();
-  uint32_t qf[SL][HD / 16][4];
-#pragma unroll
-  for (int sl = 0; sl < SL; ++sl) {
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int r = sl * 16 + (lane & 15);
-      const int ch = kk * 2 + (lane >> 4);
-      ldsm_x4(qf[sl][kk][0], qf[sl][kk][1], qf[sl][kk][2], qf[sl][kk][3], &sQ[swz<HD>(r, ch)]);
-    }
-  }
+  // Q fragments are re-read from smem per sub-block (ldmatrix) instead of living in registers:
+  // keeps the 32-row variant under 255 registers without spills
 #pragma unroll
   for (int i = 0; i < NST - 1; ++i) {
     if (i < n_stage) load_stage(i);
@@ -365,15 +355,22 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
 #pragma unroll
         for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t qa[2][4];
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
+          for (int u = 0; u < 2; ++u) {
+            const int r = sl * 16 + (lane & 15);
+            const int ch = (2 * c + u) * 2 + (lane >> 4);
+            ldsm_x4(qa[u][0], qa[u][1], qa[u][2], qa[u][3], &sQ[swz<HD>(r, ch)]);
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
             uint32_t b0, b1, b2, b3;
             const int key = warp * 16 + j * 8 + (lane & 7);
             const int ch = c * 4 + (lane >> 3);
             ldsm_x4(b0, b1, b2, b3, &K[swz<HD>(key, ch)]);
-            mma16816(sc[j], qf[sl][2 * c], b0, b1);
-            mma16816(sc[j], qf[sl][2 * c + 1], b2, b3);
+            mma16816(sc[j], qa[0], b0, b1);
+            mma16816(sc[j], qa[1], b2, b3);
           }
         }
         float bm0 = -INFINITY, bm1 = -INFINITY;
@@ -486,31 +483,100 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
     *reinterpret_cast<uint32_t*>(dst) = pack2(num0 * inv, num1 * inv);
   }
-  __syncthreads();   // the next tile reuses the smem ring / merge buffers
+  __syncthreads();   // the next item reuses the smem ring / merge buffers
+  };
+
+  if (work) {
+    // persistent: items enumerated from the per-sequence tile prefix (work[s] = first tile of s)
+    const int n_items = work[n_seq] * KVH;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int kvh = it % KVH, j = it / KVH;
+      int lo = 0, hi = n_seq;   // last s with work[s] <= j
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (work[mid] <= j) lo = mid; else hi = mid;
+      }
+      do_tile(lo, kvh, j - work[lo]);
+    }
+  } else {
+    // one CTA per (kv head, sequence) walking the sequence's tiles
+    const int kvh = blockIdx.x, s = blockIdx.y;
+    for (int tile = 0; tile * ROWS < q_len[s] * G; ++tile) do_tile(s, kvh, tile);
   }
+}
+
+// work[s] = sum over earlier sequences of ceil(q_len * G / rows); work[n_seq] = total (single block)
+__global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G, int rows, int32_t* __restrict__ work) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int base = 0; base < n_seq; base += blockDim.x) {
+    const int s = base + threadIdx.x;
+    const int t = s < n_seq ? (q_len[s] * G + rows - 1) / rows : 0;
+    int incl = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int v = lane < nw ? warp_sums[lane] : 0;
+      int iv = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, iv, o);
+        if (lane >= o) iv += y;
+      }
+      if (lane < nw) warp_sums[lane] = iv - v;
+    }
+    __syncthreads();
+    const int off = carry + warp_sums[wid] + incl - t;
+    if (s < n_seq) work[s] = off;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = off + t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) work[n_seq] = carry;
 }
 
 template <int HD, int SL>
 int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
-                 void* d_out, cudaStream_t st) {
+                 void* d_out, int32_t* d_work, cudaStream_t st) {
   constexpr int ROWS = 16 * SL;
   const int ring = 2 * 3 * 64 * HD * 2;                  // K + V stages
   const int merge = 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4;
   const int smem = (ring > merge ? ring : merge) + ROWS * HD * 2;
-  static bool set = false;
-  if (!set) {
+  static int occupancy = 0;
+  if (!occupancy) {
     cudaFuncSetAttribute(k_attention2<HD, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    set = true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occupancy, k_attention2<HD, SL>, 128, smem);
+    if (occupancy < 1) occupancy = 1;
   }
   const int G = H / KVH;
-  (void)G;
-  dim3 grid(KVH, n_seq);
-  k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
-                                                (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
-                                                d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
-                                                (__nv_bfloat16*)d_out);
+  if (d_work) {
+    // persistent CTAs over the (sequence, tile, kv head) work list: no empty CTAs, long verify blocks spread
+    static int n_sm = 0;
+    if (!n_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
+    hm_count_launches(1);
+    k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
+        (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
+        d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work);
+  } else {
+    dim3 grid(KVH, n_seq);
+    k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
+                                                  (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
+                                                  d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                  (__nv_bfloat16*)d_out, n_seq, nullptr);
+  }
   return 0;
 }
 
@@ -519,7 +585,8 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
 extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                             const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                             const int32_t* d_kv_slot, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
-                            int32_t hd, int32_t max_len, float scale, void* d_out, hm_stream_t stream) {
+                            int32_t hd, int32_t max_len, float scale, void* d_out, int32_t* d_work,
+                            hm_stream_t stream) {
   if (n_seq <= 0 || max_q_len <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
   const int G = H / KVH;
@@ -532,14 +599,14 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     const bool one = max_q_len * G <= 16;
     if (hd == 128) {
       if (one) hm::launch_attn2<128, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
       else hm::launch_attn2<128, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
     } else {
       if (one) hm::launch_attn2<64, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
       else hm::launch_attn2<64, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, st);
+                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
     }
   } else if (hd == 128) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;

@@ -123,18 +123,22 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
     M = 51
     q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
 
-    def run(sq):
+    work = torch.empty(64, dtype=torch.int32, device="cuda")
+
+    def run(sq, persistent=True):
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
         out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
         meta = [i32([s[j] for s in sq]) for j in range(4)]   # keep alive across the launch
         Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
                                        meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                        meta[3].data_ptr(), len(sq), max(s[1] for s in sq), H, KVH, hd, max_len,
-                                       1.0 / np.sqrt(hd), out.data_ptr(), 0))
+                                       1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
+                                       0))
         torch.cuda.synchronize()
         return out.view(M, H, hd)
 
     out = run(seqs)
+    assert torch.equal(out, run(seqs, persistent=False))   # work-list and per-sequence schedules agree
     for (row, h), ref in _attn_ref(torch, q, kc, vc, seqs, H, KVH, hd):
         assert torch.allclose(out[row, h].float(), ref, atol=2e-2, rtol=2e-2), (row, h)
     # the verify block of seq 1 computed one row at a time must be bit-identical
