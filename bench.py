@@ -371,11 +371,13 @@ def run_rollout(args, dist, pk):
     w = Weights(cfg, dev, seed=args.seed)
     bcast_ms = None
     if world > 1:   # epoch boundary: the updated policy travels from rank 0 (NCCL over NVLink)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        W.broadcast_weights(w, src=0)
-        torch.cuda.synchronize()
-        bcast_ms = 1e3 * (time.perf_counter() - t0)
+        for _ in range(2):   # first call includes communicator setup; report the warm one
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            W.broadcast_weights(w, src=0)
+            torch.cuda.synchronize()
+            bcast_ms = 1e3 * (time.perf_counter() - t0)
     eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev)
 
     def prompt_tokens(pid):
