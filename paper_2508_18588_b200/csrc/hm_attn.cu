@@ -14,10 +14,13 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <cstring>
 
 #include "../../include/hsmodel.h"
+#include "hm_ptx.cuh"
 
 void hm_set_error(const char* msg);
+bool hm_make_tma_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 void hm_count_launches(int64_t n);
 
 namespace hm {
@@ -268,17 +271,34 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
                                                     const int32_t* __restrict__ kv_slot, int H, int KVH,
                                                     int max_len, float scale_log2,
                                                     __nv_bfloat16* __restrict__ out, int n_seq,
-                                                    const int32_t* __restrict__ work) {
+                                                    const int32_t* __restrict__ work,
+                                                    const __grid_constant__ CUtensorMap tmK,
+                                                    const __grid_constant__ CUtensorMap tmV, int use_tma) {
   constexpr int CH = HD / 8;        // 16-byte chunks per row
   constexpr int ROWS = 16 * SL;
   constexpr int KS = 64;            // keys per stage (4 warps x 16)
   constexpr int NST = 3;            // pipeline stages
   const int G = H / KVH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  extern __shared__ __align__(128) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  // TMA 128B-swizzled destinations need 1024-byte alignment (the launch adds 1 KB of slack)
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   uint4* sK = reinterpret_cast<uint4*>(sm);            // [NST][KS][CH]
   uint4* sV = sK + NST * KS * CH;                        // [NST][KS][CH]
   uint4* sQ = sV + NST * KS * CH;                        // [ROWS][CH]
+  __shared__ uint64_t full[NST];                         // TMA stage barriers
+  const bool tma = use_tma != 0;
+  // K/V tile layout: TMA writes 64-key x 128 B halves with the hardware 128B swizzle
+  // (16-byte chunk ^ row%8); the cp.async path uses the equivalent per-row XOR on 256 B rows
+  auto kvoff = [&](int r, int ch) -> int {
+    return tma ? (ch >> 3) * (KS * 8) + r * 8 + ((ch & 7) ^ (r & 7)) : swz<HD>(r, ch);
+  };
+  if (tma && threadIdx.x == 0) {
+    for (int b = 0; b < NST; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t g_stage = 0;   // CTA-wide count of consumed TMA stages (mbarrier phase tracking)
 
   // one work item = (sequence, row tile, kv head)
   auto do_tile = [&](const int s, const int kvh, const int tile) {
@@ -301,7 +321,21 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   const __nv_bfloat16* kbase = kc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
   const __nv_bfloat16* vbase = vc + (size_t)kv_slot[s] * slot_stride + (size_t)kvh * max_len * HD;
 
+  const int row0 = (kv_slot[s] * KVH + kvh) * max_len;   // first cache row of this (slot, kv head)
+  const uint32_t g0 = g_stage;
   auto load_stage = [&](int st) {
+    if (tma) {
+      // one thread: 2 (HD=64) or 4 (HD=128) TMA boxes of 64 keys x 64 dims, completing on full[buf]
+      const int buf = (g0 + st) % NST;
+      constexpr uint32_t bytes = 2 * KS * HD * 2;
+      mbar_arrive_expect_tx(&full[buf], bytes);
+#pragma unroll
+      for (int h = 0; h < HD / 64; ++h) {
+        tma_load_2d(&tmK, &full[buf], &sK[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
+        tma_load_2d(&tmV, &full[buf], &sV[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
+      }
+      return;
+    }
     const int buf = st % NST;
     for (int c = threadIdx.x; c < KS * CH; c += blockDim.x) {
       const int r = c / CH, ch = c % CH;
@@ -317,8 +351,12 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   // keeps the 32-row variant under 255 registers without spills
 #pragma unroll
   for (int i = 0; i < NST - 1; ++i) {
-    if (i < n_stage) load_stage(i);
-    cp_commit();
+    if (tma) {
+      if (threadIdx.x == 0 && i < n_stage) load_stage(i);
+    } else {
+      if (i < n_stage) load_stage(i);
+      cp_commit();
+    }
   }
   int rpos[SL][2];
 #pragma unroll
@@ -340,11 +378,19 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   }
 
   for (int st = 0; st < n_stage; ++st) {
-    cp_wait<NST - 2>();      // stage st landed (this thread's copies)
-    __syncthreads();         // ... and everyone's; stage st-1's buffer is free again
-    if (st + NST - 1 < n_stage) load_stage(st + NST - 1);
-    cp_commit();
-    const int buf = st % NST;
+    int buf;
+    if (tma) {
+      __syncthreads();       // every warp is done with the buffer the next load overwrites
+      if (threadIdx.x == 0 && st + NST - 1 < n_stage) load_stage(st + NST - 1);
+      buf = (g0 + st) % NST;
+      mbar_wait(&full[buf], ((g0 + st) / NST) & 1);
+    } else {
+      cp_wait<NST - 2>();      // stage st landed (this thread's copies)
+      __syncthreads();         // ... and everyone's; stage st-1's buffer is free again
+      if (st + NST - 1 < n_stage) load_stage(st + NST - 1);
+      cp_commit();
+      buf = st % NST;
+    }
     const int key0 = st * KS + warp * 16;
     if (key0 <= max_pos) {   // warp-uniform
       const uint4* K = sK + (buf * KS) * CH;
@@ -368,7 +414,7 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
             uint32_t b0, b1, b2, b3;
             const int key = warp * 16 + j * 8 + (lane & 7);
             const int ch = c * 4 + (lane >> 3);
-            ldsm_x4(b0, b1, b2, b3, &K[swz<HD>(key, ch)]);
+            ldsm_x4(b0, b1, b2, b3, &K[kvoff(key, ch)]);
             mma16816(sc[j], qa[0], b0, b1);
             mma16816(sc[j], qa[1], b2, b3);
           }
@@ -430,7 +476,7 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
           uint32_t b0, b1, b2, b3;
           const int key = warp * 16 + (lane & 15);
           const int ch = n * 2 + (lane >> 4);
-          ldsm_x4_t(b0, b1, b2, b3, &V[swz<HD>(key, ch)]);
+          ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(key, ch)]);
           mma16816(o[sl][2 * n], pa, b0, b1);
           mma16816(o[sl][2 * n + 1], pa, b2, b3);
         }
@@ -439,6 +485,7 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   }
   cp_wait<0>();
   __syncthreads();
+  g_stage = g0 + n_stage;
 
   // ---- merge the 4 warps' partial states in warp order (smem reuses the K/V ring)
   float* cO = reinterpret_cast<float*>(sm);                  // [4][ROWS][HD]
@@ -545,11 +592,20 @@ template <int HD, int SL>
 int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
-                 void* d_out, int32_t* d_work, cudaStream_t st) {
+                 void* d_out, int32_t* d_work, int32_t n_slots, cudaStream_t st) {
   constexpr int ROWS = 16 * SL;
   const int ring = 2 * 3 * 64 * HD * 2;                  // K + V stages
   const int merge = 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4;
-  const int smem = (ring > merge ? ring : merge) + ROWS * HD * 2;
+  const int smem = (ring > merge ? ring : merge) + ROWS * HD * 2 + 1024;
+  // K/V caches as 2-D [slots * kv_heads * max_len, hd] bf16 tensors for TMA (rows past the end read as 0)
+  CUtensorMap mk, mv;
+  memset(&mk, 0, sizeof(mk));
+  memset(&mv, 0, sizeof(mv));
+  int use_tma = 0;
+  if (n_slots > 0 && getenv("HM_ATTN_NO_TMA") == nullptr) {
+    const int64_t rows = (int64_t)n_slots * KVH * max_len;
+    use_tma = hm_make_tma_map(&mk, d_kcache, rows, HD, HD, 64) && hm_make_tma_map(&mv, d_vcache, rows, HD, HD, 64);
+  }
   static int occupancy = 0;
   if (!occupancy) {
     cudaFuncSetAttribute(k_attention2<HD, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -569,13 +625,14 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
     hm_count_launches(1);
     k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
-        d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work);
+        d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
+        mk, mv, use_tma);
   } else {
     dim3 grid(KVH, n_seq);
     k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                   (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
                                                   d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
-                                                  (__nv_bfloat16*)d_out, n_seq, nullptr);
+                                                  (__nv_bfloat16*)d_out, n_seq, nullptr, mk, mv, use_tma);
   }
   return 0;
 }
@@ -586,7 +643,7 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
                             const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                             const int32_t* d_kv_slot, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                             int32_t hd, int32_t max_len, float scale, void* d_out, int32_t* d_work,
-                            hm_stream_t stream) {
+                            int32_t n_slots, hm_stream_t stream) {
   if (n_seq <= 0 || max_q_len <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
   const int G = H / KVH;
@@ -599,14 +656,14 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     const bool one = max_q_len * G <= 16;
     if (hd == 128) {
       if (one) hm::launch_attn2<128, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
+                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
       else hm::launch_attn2<128, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
+                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
     } else {
       if (one) hm::launch_attn2<64, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
+                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
       else hm::launch_attn2<64, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, st);
+                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
     }
   } else if (hd == 128) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;

@@ -350,6 +350,14 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int6
 
 int g_num_sms = 0;
 
+}  // namespace
+
+bool hm_make_tma_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  return make_map(m, base, rows, cols, ld, box_rows);
+}
+
+namespace {
+
 template <int BN, int kStages, int EPI>
 int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p, cudaStream_t st) {
   using C = hm::Cfg<BN, kStages>;

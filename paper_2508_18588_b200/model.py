@@ -37,7 +37,7 @@ SIGNATURES = {
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
-    "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _P],
+    "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _P],
     "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
 EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX, EPI_F32 = 0, 1, 2, 3, 4
@@ -270,7 +270,8 @@ class Forward:
                                                   q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
                                                   kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
-                                                  self.attn.data_ptr(), self.attn_work.data_ptr(), st))
+                                                  self.attn.data_ptr(), self.attn_work.data_ptr(),
+                                                  self.cache.n_slots, st))
             k("gemm_o", lambda: L.hm_gemm(EPI_F32, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
                                           M, d, hd_all, None, None, 0, y, d, None, None, mp, st))
             k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, layer["ln2"].data_ptr(), M, d, cfg.eps,

@@ -125,7 +125,7 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
 
     work = torch.empty(64, dtype=torch.int32, device="cuda")
 
-    def run(sq, persistent=True):
+    def run(sq, persistent=True, tma=True):
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
         out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
         meta = [i32([s[j] for s in sq]) for j in range(4)]   # keep alive across the launch
@@ -133,12 +133,13 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
                                        meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                        meta[3].data_ptr(), len(sq), max(s[1] for s in sq), H, KVH, hd, max_len,
                                        1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
-                                       0))
+                                       slots if tma else 0, 0))
         torch.cuda.synchronize()
         return out.view(M, H, hd)
 
     out = run(seqs)
     assert torch.equal(out, run(seqs, persistent=False))   # work-list and per-sequence schedules agree
+    assert torch.equal(out, run(seqs, tma=False))          # TMA-fed and cp.async-fed K/V stages agree
     for (row, h), ref in _attn_ref(torch, q, kc, vc, seqs, H, KVH, hd):
         assert torch.allclose(out[row, h].float(), ref, atol=2e-2, rtol=2e-2), (row, h)
     # the verify block of seq 1 computed one row at a time must be bit-identical
