@@ -13,11 +13,10 @@ namespace acc {
 __device__ __forceinline__ void probe(const HsIndexView& V, int32_t slot, int32_t m, int32_t pre_j,
                                       int32_t* pos_out, bool* found_out) {
   const int lane = lane_id();
-  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
-  for (int j = 0; j < m; ++j) {
-    int32_t t = __shfl_sync(0xffffffffu, pre_j, j);
-    h = mix64(h ^ ((uint64_t)(uint32_t)t * 0x9E3779B97F4A7C15ULL));
-  }
+  uint64_t term = lane < m ? gram_term(pre_j, lane) : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+  const uint64_t h = mix64(gram_seed(slot, m) + term);
   const int32_t tag = gram_tag(h, m);
   const int64_t lo = V.slot_text_off[slot], hi = V.slot_text_off[slot + 1];
   int64_t base = (int64_t)(h & (uint64_t)V.table_mask);

@@ -28,10 +28,29 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-__host__ __device__ __forceinline__ uint64_t gram_hash(int32_t slot, int32_t m, const int32_t* tok) {
-  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
-  for (int j = 0; j < m; ++j) h = mix64(h ^ ((uint64_t)(uint32_t)tok[j] * 0x9E3779B97F4A7C15ULL));
-  return h;
+// Polynomial gram hash: mix64(seed(slot, m) + sum_j (tok_j + 1) * P^(j+1)) mod 2^64.
+// Each term depends on one token only, so a warp / lane group computes the terms
+// in parallel and reduces them with shuffles (order independent mod 2^64).
+constexpr uint64_t kHashP = 0x9E3779B97F4A7C15ULL;
+struct PowTable {
+  uint64_t v[HS_MAX_TABLE_PREFIX];
+  constexpr PowTable() : v() {
+    uint64_t p = kHashP;
+    for (int i = 0; i < HS_MAX_TABLE_PREFIX; ++i) { v[i] = p; p *= kHashP; }
+  }
+};
+static __constant__ PowTable kPow = PowTable();
+
+__host__ __device__ __forceinline__ uint64_t gram_seed(int32_t slot, int32_t m) {
+  return mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
+}
+__device__ __forceinline__ uint64_t gram_term(int32_t tok, int j) {
+  return (uint64_t)((uint32_t)tok + 1u) * kPow.v[j];
+}
+__device__ __forceinline__ uint64_t gram_hash(int32_t slot, int32_t m, const int32_t* tok) {
+  uint64_t s = 0;
+  for (int j = 0; j < m; ++j) s += gram_term(tok[j], j);
+  return mix64(gram_seed(slot, m) + s);
 }
 
 // Hash-table tag: high bits of the hash with m in the low 6 bits.

@@ -26,11 +26,11 @@ struct Hit {
 __device__ __forceinline__ Hit probe_table(const HsIndexView& V, int32_t slot, int32_t m, int32_t pre_j) {
   const int lane = lane_id();
   // every lane computes the same hash from broadcast tokens
-  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
-  for (int j = 0; j < m; ++j) {
-    int32_t t = __shfl_sync(0xffffffffu, pre_j, j);
-    h = mix64(h ^ ((uint64_t)(uint32_t)t * 0x9E3779B97F4A7C15ULL));
-  }
+  // polynomial hash: lane j contributes term j, butterfly-summed across the warp
+  uint64_t term = lane < m ? gram_term(pre_j, lane) : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+  const uint64_t h = mix64(gram_seed(slot, m) + term);
   const int32_t tag = gram_tag(h, m);
   const int64_t lo = V.slot_text_off[slot], hi = V.slot_text_off[slot + 1];
   int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
@@ -244,11 +244,11 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
   int32_t pre_j = 0;
   if (look && j < m) pre_j = gen_tok[s * (int64_t)gen_stride + pos - m + j];
   // hash (identical in every lane of the group)
-  uint64_t h = mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
-  for (int k = 0; k < 8; ++k) {
-    int32_t t = __shfl_sync(0xffffffffu, pre_j, (g << 3) + k);
-    if (k < m) h = mix64(h ^ ((uint64_t)(uint32_t)t * 0x9E3779B97F4A7C15ULL));
-  }
+  // polynomial hash: lane j of the group contributes term j; 3-step butterfly inside the 8 lanes
+  uint64_t term = (look && j < m) ? gram_term(pre_j, j) : 0ull;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+  const uint64_t h = mix64(gram_seed(slot, m) + term);
   const int32_t tag = gram_tag(h, m);
   int32_t hit_pos = -1;
   bool done = !look;
