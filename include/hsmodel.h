@@ -89,7 +89,12 @@ int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, in
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t hd, int32_t max_len,
                  float scale, void* d_out, int32_t* d_work /* [n_seq+1] scratch or NULL */,
+                 int32_t work_ready /* d_work already holds hm_attention_plan's output */,
                  int32_t n_slots /* cache slots, > 0 enables TMA loads */, hm_stream_t stream);
+
+/* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent). */
+int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
+                      int32_t* d_work, hm_stream_t stream);
 
 /* Verify-batch assembly for the rollout step: for each live sequence s
  * (gen_len < target_len) rows [last generated token, draft_1..draft_k] at

@@ -592,7 +592,7 @@ template <int HD, int SL>
 int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
-                 void* d_out, int32_t* d_work, int32_t n_slots, cudaStream_t st) {
+                 void* d_out, int32_t* d_work, int32_t n_slots, int work_ready, cudaStream_t st) {
   constexpr int ROWS = 16 * SL;
   const int ring = 2 * 3 * 64 * HD * 2;                  // K + V stages
   const int merge = 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4;
@@ -621,8 +621,10 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
-    k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
-    hm_count_launches(1);
+    if (!work_ready) {
+      k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
+      hm_count_launches(1);
+    }
     k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
         d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
@@ -639,11 +641,26 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
 
 }  // namespace hm
 
+// Work list of the persistent attention kernel, computed once per forward (q_len is the same for
+// every layer): work[s] = first tile of sequence s, work[n_seq] = total tiles.
+extern "C" int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
+                                 int32_t* d_work, hm_stream_t stream) {
+  if (n_seq <= 0) return HM_OK;
+  if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
+  const int G = H / KVH;
+  const int rows = max_q_len * G <= 16 ? 16 : 32;   // must match the tile height chosen in hm_attention
+  hm::k_attn_tiles<<<1, 1024, 0, (cudaStream_t)stream>>>(d_q_len, n_seq, G, rows, d_work);
+  hm_count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }
+  return HM_OK;
+}
+
 extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                             const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                             const int32_t* d_kv_slot, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                             int32_t hd, int32_t max_len, float scale, void* d_out, int32_t* d_work,
-                            int32_t n_slots, hm_stream_t stream) {
+                            int32_t work_ready, int32_t n_slots, hm_stream_t stream) {
   if (n_seq <= 0 || max_q_len <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
   const int G = H / KVH;
@@ -656,14 +673,14 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     const bool one = max_q_len * G <= 16;
     if (hd == 128) {
       if (one) hm::launch_attn2<128, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
+                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
       else hm::launch_attn2<128, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
+                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
     } else {
       if (one) hm::launch_attn2<64, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
+                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
       else hm::launch_attn2<64, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, st);
+                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
     }
   } else if (hd == 128) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;

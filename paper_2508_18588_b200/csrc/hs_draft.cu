@@ -251,7 +251,6 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
   const uint64_t h = mix64(gram_seed(slot, m) + term);
   const int32_t tag = gram_tag(h, m);
   int32_t hit_pos = -1;
-  int32_t t4[4] = {0, 0, 0, 0};   // draft tokens text[hit_pos + m + r*8 + j]
   bool done = !look;
   int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
   const int64_t lo = look ? V.slot_text_off[slot] : 0, hi = look ? V.slot_text_off[slot + 1] : 0;
@@ -267,28 +266,16 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
     unsigned cm = (__ballot_sync(0xffffffffu, cand) & gmask) >> (g * 8);
     unsigned live = em ? ((1u << (__ffs(em) - 1)) - 1u) : 0xFFu;
     cm &= live;
-    // verify candidates in probe order (rare: at most a couple per query); the draft tokens of
-    // the candidate are loaded in the same round trip as the verify tokens
+    // verify candidates in probe order (rare: at most a couple per query)
     while (__any_sync(0xffffffffu, cm != 0)) {
       const int src = cm ? (g << 3) + __ffs(cm) - 1 : lane;
       const int32_t cpos = __shfl_sync(0xffffffffu, e.pos, src);
       bool bad = false;
-      int32_t c4[4];
-      if (cm) {
-        const int32_t vt = j < m ? V.text[cpos + j] : 0;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int idx = r * 8 + j;
-          c4[r] = idx < win ? V.text[cpos + m + idx] : 0;
-        }
-        bad = j < m && vt != pre_j;
-      }
+      if (cm && j < m) bad = V.text[cpos + j] != pre_j;
       unsigned bm = (__ballot_sync(0xffffffffu, bad) & gmask);
       if (cm) {
         if (!bm) {
           hit_pos = cpos;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) t4[r] = c4[r];
           cm = 0;
           em = 1;   // resolved
         } else {
@@ -300,11 +287,13 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
     base += 8;
   }
   const bool hit = hit_pos >= 0;
-  // cut the draft at the first terminal
+  // draft: tokens text[hit_pos + m + r*8 + j], r = 0..3, cut at the first terminal
+  int32_t t4[4];
   int32_t first_term = 32;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int idx = r * 8 + j;
+    t4[r] = (hit && idx < win) ? V.text[hit_pos + m + idx] : 0;
     if (hit && idx < win && t4[r] < 0 && idx < first_term) first_term = idx;
   }
   // group min of first_term

@@ -37,7 +37,9 @@ SIGNATURES = {
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
-    "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _P],
+    "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _I32,
+                     _P],
+    "hm_attention_plan": [_P, _I32, _I32, _I32, _I32, _P, _P],
     "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
 EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX, EPI_F32 = 0, 1, 2, 3, 4
@@ -253,6 +255,8 @@ class Forward:
         k("embed", lambda: L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
         hd_all = cfg.n_heads * cfg.head_dim
         y = self.y.data_ptr()
+        k("attn_plan", lambda: L.hm_attention_plan(q_len.data_ptr(), n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads,
+                                                   self.attn_work.data_ptr(), st))
         for li, layer in enumerate(w.layers):
             kc, vc = self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr()
             # x += y (previous down-proj; none before layer 0), h = rmsnorm(x)
@@ -270,7 +274,7 @@ class Forward:
                                                   q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
                                                   kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
-                                                  self.attn.data_ptr(), self.attn_work.data_ptr(),
+                                                  self.attn.data_ptr(), self.attn_work.data_ptr(), 1,
                                                   self.cache.n_slots, st))
             k("gemm_o", lambda: L.hm_gemm(EPI_F32, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
                                           M, d, hd_all, None, None, 0, y, d, None, None, mp, st))

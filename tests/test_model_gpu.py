@@ -133,7 +133,7 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
                                        meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                        meta[3].data_ptr(), len(sq), max(s[1] for s in sq), H, KVH, hd, max_len,
                                        1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
-                                       slots if tma else 0, 0))
+                                       0, slots if tma else 0, 0))
         torch.cuda.synchronize()
         return out.view(M, H, hd)
 
