@@ -10,6 +10,8 @@
 // binary search over the slot's suffix array with warp-parallel comparisons,
 // then the locus node from a warp min-scan of the LCP values inside the
 // interval.
+#include <cstdlib>
+
 #include "hs_common.cuh"
 
 namespace hs {
@@ -222,7 +224,14 @@ __global__ void __launch_bounds__(256) k_draft(HsIndexView V, int32_t n_seq, con
 // lane j holds prefix token j, probes table entry base + j (8 x 16 B = one
 // 128 B line), verifies a tag hit with one compare per lane + group ballot,
 // and reads/writes the draft as 4 coalesced 32 B rows (tokens j, j+8, ...).
-__global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, const int32_t* __restrict__ slot_of_seq,
+//
+// FUSED (default): the common case -- the first probed row holds the key --
+// is resolved in one round trip after the table load: the first live
+// candidate's verify tokens text[pos + j] and draft tokens text[pos + m + ...]
+// are requested together; only groups whose first candidate fails (or whose
+// key lies beyond the first row) take the general probe loop.
+template <bool FUSED>
+__global__ void __launch_bounds__(256, 8) k_draft8(HsIndexView V, int32_t n_seq, const int32_t* __restrict__ slot_of_seq,
                                                 const int32_t* __restrict__ gen_tok, int32_t gen_stride,
                                                 const int32_t* __restrict__ gen_len,
                                                 const int32_t* __restrict__ prefix_len,
@@ -254,6 +263,36 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
   bool done = !look;
   int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
   const int64_t lo = look ? V.slot_text_off[slot] : 0, hi = look ? V.slot_text_off[slot + 1] : 0;
+  int32_t t4[4] = {0, 0, 0, 0};   // draft tokens text[hit_pos + m + r*8 + j]
+  bool have_t4 = false;
+  if (FUSED) {
+    HsGramEntry e;
+    e.pos = -1;
+    e.tag = 0;
+    if (look) e = V.table[(base + j) & V.table_mask];
+    const bool empty = look && e.pos < 0;
+    const bool cand = look && !empty && e.tag == tag && e.pos >= lo && e.pos < hi;
+    const unsigned em = (__ballot_sync(0xffffffffu, empty) & gmask) >> (g * 8);
+    unsigned cm = (__ballot_sync(0xffffffffu, cand) & gmask) >> (g * 8);
+    cm &= em ? ((1u << (__ffs(em) - 1)) - 1u) : 0xFFu;
+    const int src = cm ? (g << 3) + __ffs(cm) - 1 : lane;
+    const int32_t cpos = __shfl_sync(0xffffffffu, e.pos, src);
+    int32_t vt = 0;
+    if (cm) {
+      vt = j < m ? V.text[cpos + j] : 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) t4[r] = r * 8 + j < win ? V.text[cpos + m + r * 8 + j] : 0;
+    }
+    const unsigned bm = __ballot_sync(0xffffffffu, cm && j < m && vt != pre_j) & gmask;
+    if (cm && !bm) {
+      hit_pos = cpos;
+      have_t4 = true;
+      done = true;
+    } else if (!cm && em) {
+      done = true;   // an empty slot before any candidate: the key is absent
+    }
+    // unresolved groups rescan from the first row in the general loop below
+  }
   // probe loop: every group iterates until it resolves (warp-uniform trip via __any_sync)
   while (__any_sync(0xffffffffu, !done)) {
     HsGramEntry e;
@@ -288,12 +327,14 @@ __global__ void __launch_bounds__(256) k_draft8(HsIndexView V, int32_t n_seq, co
   }
   const bool hit = hit_pos >= 0;
   // draft: tokens text[hit_pos + m + r*8 + j], r = 0..3, cut at the first terminal
-  int32_t t4[4];
+  if (hit && !have_t4) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) t4[r] = r * 8 + j < win ? V.text[hit_pos + m + r * 8 + j] : 0;
+  }
   int32_t first_term = 32;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int idx = r * 8 + j;
-    t4[r] = (hit && idx < win) ? V.text[hit_pos + m + idx] : 0;
     if (hit && idx < win && t4[r] < 0 && idx < first_term) first_term = idx;
   }
   // group min of first_term
@@ -356,10 +397,12 @@ extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d
     int64_t warps = ((int64_t)n_seq + 3) / 4;
     int64_t blocks8 = (warps * 32 + threads - 1) / threads;
     hs_count_launches(1);
-    k_draft8<<<(unsigned)blocks8, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
-                                                                     d_gen_len, d_prefix_len, d_window, d_speculate,
-                                                                     d_draft_tok, draft_stride, d_draft_len, d_looked,
-                                                                     d_found);
+    static const bool unfused = getenv("HS_K2_UNFUSED") != nullptr;   // A/B switch for profiling only
+    auto kern = unfused ? k_draft8<false> : k_draft8<true>;
+    kern<<<(unsigned)blocks8, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
+                                                                  d_gen_len, d_prefix_len, d_window, d_speculate,
+                                                                  d_draft_tok, draft_stride, d_draft_len, d_looked,
+                                                                  d_found);
     HS_CUDA_TRY(cudaGetLastError());
     return HS_OK;
   }

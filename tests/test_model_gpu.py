@@ -148,6 +148,48 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
         assert torch.equal(single[1 + i], out[1 + i])
 
 
+@pytest.mark.gpu
+def test_attention_many_items_per_cta(torch):
+    """Several work items per persistent CTA (the warp-specialised verify kernel's
+    producer runs ahead across items and wraps the stage ring many times):
+    identical to the per-sequence schedule and to one-row-at-a-time decode."""
+    import paper_2508_18588_b200.model as Mo
+    H, KVH, hd = 12, 2, 128
+    rng = np.random.default_rng(5)
+    n, slots, max_len = 700, 700, 640
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kc = torch.randn(slots, KVH, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(slots, KVH, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    q_len = rng.integers(1, 34, size=n)
+    q_off = np.concatenate([[0], np.cumsum(q_len)[:-1]])
+    pos0 = rng.integers(0, max_len - 34, size=n)
+    M = int(q_len.sum())
+    q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+    work = torch.empty(M + 1, dtype=torch.int32, device="cuda")   # [n_seq + 1] for the decode run below
+    i32 = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32)).cuda()  # noqa: E731
+
+    def run(qo, ql, p0, sl, persistent):
+        out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
+        meta = [i32(qo), i32(ql), i32(p0), i32(sl)]
+        Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+                                       meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
+                                       meta[3].data_ptr(), len(ql), int(max(ql)), H, KVH, hd, max_len,
+                                       1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
+                                       0, slots, 0))
+        torch.cuda.synchronize()
+        return out
+
+    slot = np.arange(n)
+    a = run(q_off, q_len, pos0, slot, True)
+    b = run(q_off, q_len, pos0, slot, False)
+    assert torch.equal(a, b)
+    # every row as its own decode query (q_len 1: the 16-row decode kernel)
+    rows = np.arange(M)
+    seq_of_row = np.repeat(np.arange(n), q_len)
+    dec = run(rows, np.ones(M), pos0[seq_of_row] + rows - q_off[seq_of_row], slot[seq_of_row], True)
+    assert torch.equal(a, dec)
+
+
 def test_tiny_forward_logits_vs_reference(torch):
     from oracle import model_ref as R
     from paper_2508_18588_b200.model import TINY, Forward, KVCache, Weights
