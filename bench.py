@@ -446,9 +446,11 @@ def run_rollout(args, dist, pk):
     bytes_total = res.forwards * res.weight_bytes + res.kv_bytes
     t_roof = max(bytes_total / (pk["hbm_gbs"] * 1e9), res.flops / (pk["bf16_tflops_sustained"] * 1e12))
     # dominant kernel, timed live with CUDA events in a representative verify forward
-    live_iters = float(st[3] + st[4])
-    q_mean = max(1, int(round((res.rows - B * P) / max(live_iters - B, 1))))
-    prof, M = profile_forward(eng, B, P + T // 2, q_mean)
+    # verify-block sizes drawn from this run's own (sequence, iteration) histogram
+    qh = res.qlen_hist.astype(np.float64)
+    q_lens = np.random.default_rng([args.seed, 77]).choice(len(qh), size=B, p=qh / qh.sum()).astype(np.int32)
+    q_mean = float(q_lens.mean())
+    prof, M = profile_forward(eng, B, P + T // 2, q_lens)
     label, (k_ms, k_n) = max(prof.items(), key=lambda kv: kv[1][0])
     shapes = eng.fwd.gemm_shapes()
     kernels = {}
@@ -466,7 +468,7 @@ def run_rollout(args, dist, pk):
                 "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": None,
                 "per_launch_flops": 2.0 * M * N_ * K_, "M": M, "N": N_, "K": K_}
     else:   # attention: KV bytes
-        kvb = B * (P + T // 2 + q_mean) * cfg.n_kv_heads * cfg.head_dim * 2 * 2 * k_n
+        kvb = float((P + T // 2 + q_lens).sum()) * cfg.n_kv_heads * cfg.head_dim * 2 * 2 * k_n
         ach = kvb / (k_ms / 1e3) / 1e9
         roof = {"kernel": label, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "traffic": None}
@@ -506,7 +508,10 @@ def run_rollout(args, dist, pk):
                           "flops": res.flops, "bytes": bytes_total, "note": "aggregate bound max(sum bytes/HBM, "
                           "sum flops/sustained bf16) <= sum of per-forward maxima"},
         "kernels_ms_per_forward": kernels,
-        "profiled_forward": {"seqs": B, "rows_per_seq": q_mean, "ctx": P + T // 2, "M": M},
+        "profiled_forward": {"seqs": B, "rows_per_seq_mean": q_mean, "rows_per_seq_max": int(q_lens.max()),
+                             "ctx": P + T // 2, "M": M,
+                             "note": "verify-block sizes sampled from this run's histogram"},
+        "verify_rows_hist": {str(i): int(c) for i, c in enumerate(res.qlen_hist) if c},
         "clocks": clocks,
     }
     return line, {"cfg": cfg, "prompts": prompts, "T": T, "w": w}

@@ -15,6 +15,7 @@
 #include <stdint.h>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "../../include/hsmodel.h"
 #include "hm_ptx.cuh"
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
                                                     __nv_bfloat16* __restrict__ out, int n_seq,
                                                     const int32_t* __restrict__ work,
                                                     const __grid_constant__ CUtensorMap tmK,
-                                                    const __grid_constant__ CUtensorMap tmV, int use_tma) {
+                                                    const __grid_constant__ CUtensorMap tmV, int use_tma, int flags) {
   constexpr int CH = HD / 8;        // 16-byte chunks per row
   constexpr int ROWS = 16 * SL;
   constexpr int KS = 64;            // keys per stage (4 warps x 16)
@@ -359,6 +360,11 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     }
   }
   int rpos[SL][2];
+  // per slice: live (any row < rows_total; a slice of padding rows only is skipped -- its state is
+  // never merged into an output row) and vis_all (keys <= vis_all are visible to all 16 rows, so
+  // their blocks skip the mask: the mask is the identity there).  Both warp-uniform, both exact.
+  bool live[SL];
+  int vis_all[SL];
 #pragma unroll
   for (int sl = 0; sl < SL; ++sl) {
 #pragma unroll
@@ -366,6 +372,9 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
       const int rr = tile * ROWS + sl * 16 + (lane >> 2) + 8 * h;
       rpos[sl][h] = rr < rows_total ? p0 + rr / G : -1;   // -1: padding row, fully masked
     }
+    const int first = tile * ROWS + sl * 16;
+    live[sl] = first < rows_total;
+    vis_all[sl] = first + 15 < rows_total ? p0 + first / G : -1;
   }
   float o[SL][HD / 8][4];
   float mrow[SL][2], lrow[SL][2];
@@ -377,58 +386,81 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     lrow[sl][0] = lrow[sl][1] = 0.f;
   }
 
-  for (int st = 0; st < n_stage; ++st) {
-    int buf;
-    if (tma) {
-      __syncthreads();       // every warp is done with the buffer the next load overwrites
-      if (threadIdx.x == 0 && st + NST - 1 < n_stage) load_stage(st + NST - 1);
-      buf = (g0 + st) % NST;
-      mbar_wait(&full[buf], ((g0 + st) / NST) & 1);
-    } else {
-      cp_wait<NST - 2>();      // stage st landed (this thread's copies)
-      __syncthreads();         // ... and everyone's; stage st-1's buffer is free again
-      if (st + NST - 1 < n_stage) load_stage(st + NST - 1);
-      cp_commit();
-      buf = st % NST;
-    }
-    const int key0 = st * KS + warp * 16;
-    if (key0 <= max_pos) {   // warp-uniform
+  // The stage loop, instantiated for the number NS of live 16-row slices of this tile (trailing
+  // slices of padding rows only are skipped: their state never reaches an output row).  The live
+  // slices share every K and V fragment load, and their independent mma/softmax chains interleave.
+  // Per slice the arithmetic is identical for every NS and SL (a row's bits do not depend on the tile).
+  auto stages = [&](auto ns_tag) {
+    constexpr int NS = decltype(ns_tag)::value;
+    for (int st = 0; st < n_stage; ++st) {
+      int buf;
+      if (tma) {
+        __syncthreads();       // every warp is done with the buffer the next load overwrites
+        if (threadIdx.x == 0 && st + NST - 1 < n_stage) load_stage(st + NST - 1);
+        buf = (g0 + st) % NST;
+        mbar_wait(&full[buf], ((g0 + st) / NST) & 1);
+      } else {
+        cp_wait<NST - 2>();      // stage st landed (this thread's copies)
+        __syncthreads();         // ... and everyone's; stage st-1's buffer is free again
+        if (st + NST - 1 < n_stage) load_stage(st + NST - 1);
+        cp_commit();
+        buf = st % NST;
+      }
+      const int key0 = st * KS + warp * 16;
+      if (key0 > max_pos) continue;   // warp-uniform
       const uint4* K = sK + (buf * KS) * CH;
       const uint4* V = sV + (buf * KS) * CH;
+      float sc[NS][2][4];
 #pragma unroll
-      for (int sl = 0; sl < SL; ++sl) {
-        float sc[2][4];
+      for (int sl = 0; sl < NS; ++sl)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+        for (int j = 0; j < 2; ++j) sc[sl][j][0] = sc[sl][j][1] = sc[sl][j][2] = sc[sl][j][3] = 0.f;
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t kb[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          ldsm_x4(kb[j][0], kb[j][1], kb[j][2], kb[j][3], &K[kvoff(warp * 16 + j * 8 + (lane & 7), c * 4 + (lane >> 3))]);
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
           uint32_t qa[2][4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int r = sl * 16 + (lane & 15);
-            const int ch = (2 * c + u) * 2 + (lane >> 4);
-            ldsm_x4(qa[u][0], qa[u][1], qa[u][2], qa[u][3], &sQ[swz<HD>(r, ch)]);
-          }
+          for (int u = 0; u < 2; ++u)
+            ldsm_x4(qa[u][0], qa[u][1], qa[u][2], qa[u][3],
+                    &sQ[swz<HD>(sl * 16 + (lane & 15), (2 * c + u) * 2 + (lane >> 4))]);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            uint32_t b0, b1, b2, b3;
-            const int key = warp * 16 + j * 8 + (lane & 7);
-            const int ch = c * 4 + (lane >> 3);
-            ldsm_x4(b0, b1, b2, b3, &K[kvoff(key, ch)]);
-            mma16816(sc[j], qa[0], b0, b1);
-            mma16816(sc[j], qa[1], b2, b3);
+            mma16816(sc[sl][j], qa[0], kb[j][0], kb[j][1]);
+            mma16816(sc[sl][j], qa[1], kb[j][2], kb[j][3]);
           }
         }
+      }
+      uint32_t pa[NS][4];
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
         float bm0 = -INFINITY, bm1 = -INFINITY;
+        if ((flags & 4) && key0 + 15 <= vis_all[sl]) {   // block visible to every row: the mask is the identity
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < 2; ++j) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = key0 + j * 8 + 2 * (lane & 3) + e;
-            sc[j][e] = key <= rpos[sl][0] ? sc[j][e] * scale_log2 : -INFINITY;
-            sc[j][2 + e] = key <= rpos[sl][1] ? sc[j][2 + e] * scale_log2 : -INFINITY;
-            bm0 = fmaxf(bm0, sc[j][e]);
-            bm1 = fmaxf(bm1, sc[j][2 + e]);
+            for (int e = 0; e < 2; ++e) {
+              sc[sl][j][e] *= scale_log2;
+              sc[sl][j][2 + e] *= scale_log2;
+              bm0 = fmaxf(bm0, sc[sl][j][e]);
+              bm1 = fmaxf(bm1, sc[sl][j][2 + e]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int key = key0 + j * 8 + 2 * (lane & 3) + e;
+              sc[sl][j][e] = key <= rpos[sl][0] ? sc[sl][j][e] * scale_log2 : -INFINITY;
+              sc[sl][j][2 + e] = key <= rpos[sl][1] ? sc[sl][j][2 + e] * scale_log2 : -INFINITY;
+              bm0 = fmaxf(bm0, sc[sl][j][e]);
+              bm1 = fmaxf(bm1, sc[sl][j][2 + e]);
+            }
           }
         }
         bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
@@ -443,45 +475,53 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          sc[j][0] = exp2f(sc[j][0] - sub0);
-          sc[j][1] = exp2f(sc[j][1] - sub0);
-          sc[j][2] = exp2f(sc[j][2] - sub1);
-          sc[j][3] = exp2f(sc[j][3] - sub1);
-          rs0 += sc[j][0] + sc[j][1];
-          rs1 += sc[j][2] + sc[j][3];
+          sc[sl][j][0] = exp2f(sc[sl][j][0] - sub0);
+          sc[sl][j][1] = exp2f(sc[sl][j][1] - sub0);
+          sc[sl][j][2] = exp2f(sc[sl][j][2] - sub1);
+          sc[sl][j][3] = exp2f(sc[sl][j][3] - sub1);
+          rs0 += sc[sl][j][0] + sc[sl][j][1];
+          rs1 += sc[sl][j][2] + sc[sl][j][3];
         }
         rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
         rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
         rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
         rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
-        lrow[sl][0] = __fmaf_rn(lrow[sl][0], a0, rs0);
-        lrow[sl][1] = __fmaf_rn(lrow[sl][1], a1, rs1);
+        lrow[sl][0] = lrow[sl][0] * a0 + rs0;
+        lrow[sl][1] = lrow[sl][1] * a1 + rs1;
         mrow[sl][0] = nm0;
         mrow[sl][1] = nm1;
-        uint32_t pa[4];
-        pa[0] = pack2(sc[0][0], sc[0][1]);
-        pa[1] = pack2(sc[0][2], sc[0][3]);
-        pa[2] = pack2(sc[1][0], sc[1][1]);
-        pa[3] = pack2(sc[1][2], sc[1][3]);
+        pa[sl][0] = pack2(sc[sl][0][0], sc[sl][0][1]);
+        pa[sl][1] = pack2(sc[sl][0][2], sc[sl][0][3]);
+        pa[sl][2] = pack2(sc[sl][1][0], sc[sl][1][1]);
+        pa[sl][3] = pack2(sc[sl][1][2], sc[sl][1][3]);
+        // rescale only when some row's running max moved: skipping a multiply by exactly 1 is exact
+        if (!(flags & 1) || __any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
 #pragma unroll
-        for (int n = 0; n < HD / 16; ++n) {
-          o[sl][2 * n][0] *= a0;
-          o[sl][2 * n][1] *= a0;
-          o[sl][2 * n][2] *= a1;
-          o[sl][2 * n][3] *= a1;
-          o[sl][2 * n + 1][0] *= a0;
-          o[sl][2 * n + 1][1] *= a0;
-          o[sl][2 * n + 1][2] *= a1;
-          o[sl][2 * n + 1][3] *= a1;
-          uint32_t b0, b1, b2, b3;
-          const int key = warp * 16 + (lane & 15);
-          const int ch = n * 2 + (lane >> 4);
-          ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(key, ch)]);
-          mma16816(o[sl][2 * n], pa, b0, b1);
-          mma16816(o[sl][2 * n + 1], pa, b2, b3);
+          for (int n = 0; n < HD / 8; ++n) {
+            o[sl][n][0] *= a0;
+            o[sl][n][1] *= a0;
+            o[sl][n][2] *= a1;
+            o[sl][n][3] *= a1;
+          }
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < HD / 16; ++n) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(warp * 16 + (lane & 15), n * 2 + (lane >> 4))]);
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          mma16816(o[sl][2 * n], pa[sl], b0, b1);
+          mma16816(o[sl][2 * n + 1], pa[sl], b2, b3);
         }
       }
     }
+  };
+  if constexpr (SL == 1) {
+    stages(std::integral_constant<int, 1>{});
+  } else {
+    if ((flags & 2) && !live[1]) stages(std::integral_constant<int, 1>{});
+    else stages(std::integral_constant<int, SL>{});
   }
   cp_wait<0>();
   __syncthreads();
@@ -522,9 +562,9 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     for (int w = 0; w < 4; ++w) {
       const float mw = cM[w * ROWS + r];
       const float sc = mw == -INFINITY ? 0.f : exp2f(mw - mx);
-      den = __fmaf_rn(cL[w * ROWS + r], sc, den);
-      num0 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d], sc, num0);
-      num1 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d + 1], sc, num1);
+      den += cL[w * ROWS + r] * sc;
+      num0 += cO[((size_t)w * ROWS + r) * HD + d] * sc;
+      num1 += cO[((size_t)w * ROWS + r) * HD + d + 1] * sc;
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
     __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
@@ -549,278 +589,6 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
     // one CTA per (kv head, sequence) walking the sequence's tiles
     const int kvh = blockIdx.x, s = blockIdx.y;
     for (int tile = 0; tile * ROWS < q_len[s] * G; ++tile) do_tile(s, kvh, tile);
-  }
-}
-
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-// v3 (verify blocks, 32-row tiles): warp-specialised.  Warp 8 is a TMA
-// producer that streams 64-key K/V stages into a 4-deep smem ring gated by
-// full/empty mbarriers and runs ahead across work items (the merge buffers are
-// separate from the ring, so the next item's first stages land while the
-// current one merges); warps 0-7 are consumers, warp w = (key group w & 3,
-// row slice w >> 2).  One slice per warp halves the dependent mma/softmax
-// chain per stage compared with k_attention2<HD, 2>, and no CTA-wide barrier
-// sits between stages.  Each consumer performs exactly the arithmetic of
-// k_attention2's (key group, slice) pair in the same order, and the merge is
-// the same fixed-order formula, so every row is bit-identical to the decode
-// kernel's result (greedy under speculation stays bit-exact).
-template <int HD>
-__global__ void __launch_bounds__(288, 1) k_attention3(const __nv_bfloat16* __restrict__ q,
-                                                       const int32_t* __restrict__ q_off,
-                                                       const int32_t* __restrict__ q_len,
-                                                       const int32_t* __restrict__ pos0,
-                                                       const int32_t* __restrict__ kv_slot, int H, int KVH,
-                                                       int max_len, float scale_log2,
-                                                       __nv_bfloat16* __restrict__ out, int n_seq,
-                                                       const int32_t* __restrict__ work,
-                                                       const __grid_constant__ CUtensorMap tmK,
-                                                       const __grid_constant__ CUtensorMap tmV) {
-  constexpr int CH = HD / 8;
-  constexpr int ROWS = 32;
-  constexpr int KS = 64;
-  constexpr int NST = 4;
-  const int G = H / KVH;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  extern __shared__ __align__(1024) uint8_t sm_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-  uint4* sK = reinterpret_cast<uint4*>(sm);            // [NST][KS][CH], TMA 128B swizzle
-  uint4* sV = sK + NST * KS * CH;
-  uint4* sQ = sV + NST * KS * CH;                        // [ROWS][CH]
-  float* cO = reinterpret_cast<float*>(sQ + ROWS * CH);  // [4][ROWS][HD]
-  float* cM = cO + 4 * ROWS * HD;                        // [4][ROWS]
-  float* cL = cM + 4 * ROWS;                             // [4][ROWS]
-  __shared__ uint64_t full[NST], empty[NST];
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < NST; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], 8);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int n_items = work[n_seq] * KVH;
-  auto locate = [&](int it, int& s, int& kvh, int& tile) {
-    kvh = it % KVH;
-    const int j = it / KVH;
-    int lo = 0, hi = n_seq;   // last s with work[s] <= j
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (work[mid] <= j) lo = mid; else hi = mid;
-    }
-    s = lo;
-    tile = j - work[lo];
-  };
-
-  if (warp == 8) {
-    // ---- producer: one thread walks the CTA's items and keeps the ring full
-    if (lane == 0) {
-      uint32_t g = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        int s, kvh, tile;
-        locate(it, s, kvh, tile);
-        const int rows_total = q_len[s] * G;
-        const int last_row = min(rows_total, (tile + 1) * ROWS) - 1;
-        const int n_stage = (pos0[s] + last_row / G) / KS + 1;
-        const int row0 = (kv_slot[s] * KVH + kvh) * max_len;
-        for (int st = 0; st < n_stage; ++st, ++g) {
-          const int buf = g % NST;
-          if (g >= NST) mbar_wait(&empty[buf], ((g / NST) - 1) & 1);
-          mbar_arrive_expect_tx(&full[buf], 2 * KS * HD * 2);
-#pragma unroll
-          for (int h = 0; h < HD / 64; ++h) {
-            tma_load_2d(&tmK, &full[buf], &sK[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
-            tma_load_2d(&tmV, &full[buf], &sV[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---- consumers
-  const int kg = warp & 3, sl = warp >> 2;
-  auto kvoff = [&](int r, int ch) -> int { return (ch >> 3) * (KS * 8) + r * 8 + ((ch & 7) ^ (r & 7)); };
-  uint32_t g = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    int s, kvh, tile;
-    locate(it, s, kvh, tile);
-    const int rows_total = q_len[s] * G;
-    const int qo = q_off[s], p0 = pos0[s];
-    for (int c = threadIdx.x; c < ROWS * CH; c += 256) {
-      const int r = c / CH, ch = c % CH;
-      const int rr = tile * ROWS + r;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (rr < rows_total) {
-        const int qi = rr / G, hj = kvh * G + rr % G;
-        v = reinterpret_cast<const uint4*>(q + ((size_t)(qo + qi) * H + hj) * HD)[ch];
-      }
-      sQ[swz<HD>(r, ch)] = v;
-    }
-    const int last_row = min(rows_total, (tile + 1) * ROWS) - 1;
-    const int max_pos = p0 + last_row / G;
-    const int n_stage = max_pos / KS + 1;
-    int rpos[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int rr = tile * ROWS + sl * 16 + (lane >> 2) + 8 * h;
-      rpos[h] = rr < rows_total ? p0 + rr / G : -1;
-    }
-    float o[HD / 8][4];
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-    consumer_bar();   // Q tile visible
-    // this warp's Q fragments stay in registers for the whole item (k_attention2 re-reads them per stage)
-    uint32_t qf[HD / 16][4];
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk)
-      ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], &sQ[swz<HD>(sl * 16 + (lane & 15), kk * 2 + (lane >> 4))]);
-    // keys <= vis_all are visible to all 16 rows of the slice (no padding row): their blocks skip the mask
-    const int first_rr = tile * ROWS + sl * 16;
-    const int vis_all = first_rr + 15 < rows_total ? p0 + first_rr / G : -1;
-
-    for (int st = 0; st < n_stage; ++st, ++g) {
-      const int buf = g % NST;
-      mbar_wait(&full[buf], (g / NST) & 1);
-      const int key0 = st * KS + kg * 16;
-      if (key0 <= max_pos) {
-        const uint4* K = sK + (buf * KS) * CH;
-        const uint4* V = sV + (buf * KS) * CH;
-        float sc[2][4];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            uint32_t b0, b1, b2, b3;
-            const int key = kg * 16 + j * 8 + (lane & 7);
-            const int ch = c * 4 + (lane >> 3);
-            ldsm_x4(b0, b1, b2, b3, &K[kvoff(key, ch)]);
-            mma16816(sc[j], qf[2 * c], b0, b1);
-            mma16816(sc[j], qf[2 * c + 1], b2, b3);
-          }
-        }
-        float bm0 = -INFINITY, bm1 = -INFINITY;
-        if (key0 + 15 <= vis_all) {   // warp-uniform: whole block visible, the mask is the identity
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              sc[j][e] *= scale_log2;
-              sc[j][2 + e] *= scale_log2;
-              bm0 = fmaxf(bm0, sc[j][e]);
-              bm1 = fmaxf(bm1, sc[j][2 + e]);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int key = key0 + j * 8 + 2 * (lane & 3) + e;
-              sc[j][e] = key <= rpos[0] ? sc[j][e] * scale_log2 : -INFINITY;
-              sc[j][2 + e] = key <= rpos[1] ? sc[j][2 + e] * scale_log2 : -INFINITY;
-              bm0 = fmaxf(bm0, sc[j][e]);
-              bm1 = fmaxf(bm1, sc[j][2 + e]);
-            }
-          }
-        }
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-        const float nm0 = fmaxf(mrow[0], bm0), nm1 = fmaxf(mrow[1], bm1);
-        const float a0 = nm0 == -INFINITY ? 1.f : exp2f(mrow[0] - nm0);
-        const float a1 = nm1 == -INFINITY ? 1.f : exp2f(mrow[1] - nm1);
-        const float sub0 = nm0 == -INFINITY ? 0.f : nm0;
-        const float sub1 = nm1 == -INFINITY ? 0.f : nm1;
-        float rs0 = 0.f, rs1 = 0.f;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          sc[j][0] = exp2f(sc[j][0] - sub0);
-          sc[j][1] = exp2f(sc[j][1] - sub0);
-          sc[j][2] = exp2f(sc[j][2] - sub1);
-          sc[j][3] = exp2f(sc[j][3] - sub1);
-          rs0 += sc[j][0] + sc[j][1];
-          rs1 += sc[j][2] + sc[j][3];
-        }
-        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
-        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
-        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
-        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
-        lrow[0] = __fmaf_rn(lrow[0], a0, rs0);
-        lrow[1] = __fmaf_rn(lrow[1], a1, rs1);
-        mrow[0] = nm0;
-        mrow[1] = nm1;
-        uint32_t pa[4];
-        pa[0] = pack2(sc[0][0], sc[0][1]);
-        pa[1] = pack2(sc[0][2], sc[0][3]);
-        pa[2] = pack2(sc[1][0], sc[1][1]);
-        pa[3] = pack2(sc[1][2], sc[1][3]);
-        // rescale only when some row's running max moved (a multiply by exactly 1 is skipped: bit-identical)
-        if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
-#pragma unroll
-          for (int n = 0; n < HD / 8; ++n) {
-            o[n][0] *= a0;
-            o[n][1] *= a0;
-            o[n][2] *= a1;
-            o[n][3] *= a1;
-          }
-        }
-#pragma unroll
-        for (int n = 0; n < HD / 16; ++n) {
-          uint32_t b0, b1, b2, b3;
-          const int key = kg * 16 + (lane & 15);
-          const int ch = n * 2 + (lane >> 4);
-          ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(key, ch)]);
-          mma16816(o[2 * n], pa, b0, b1);
-          mma16816(o[2 * n + 1], pa, b2, b3);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[buf]);   // this warp is done reading the stage
-    }
-
-    // ---- merge the 4 key groups' partial states in key-group order (same formula as k_attention2)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = sl * 16 + (lane >> 2) + 8 * h;
-      float* dst = cO + ((size_t)kg * ROWS + r) * HD;
-#pragma unroll
-      for (int i = 0; i < HD / 8; ++i) {
-        const int col = i * 8 + 2 * (lane & 3);
-        dst[col] = o[i][2 * h];
-        dst[col + 1] = o[i][2 * h + 1];
-      }
-      if ((lane & 3) == 0) {
-        cM[kg * ROWS + r] = mrow[h];
-        cL[kg * ROWS + r] = lrow[h];
-      }
-    }
-    consumer_bar();
-    for (int e = threadIdx.x; e < ROWS * (HD / 2); e += 256) {
-      const int r = e / (HD / 2), d = (e % (HD / 2)) * 2;
-      const int rr = tile * ROWS + r;
-      if (rr >= rows_total) continue;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) mx = fmaxf(mx, cM[w * ROWS + r]);
-      float num0 = 0.f, num1 = 0.f, den = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float mw = cM[w * ROWS + r];
-        const float sc = mw == -INFINITY ? 0.f : exp2f(mw - mx);
-        den = __fmaf_rn(cL[w * ROWS + r], sc, den);
-        num0 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d], sc, num0);
-        num1 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d + 1], sc, num1);
-      }
-      const float inv = den > 0.f ? 1.f / den : 0.f;
-      __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
-      *reinterpret_cast<uint32_t*>(dst) = pack2(num0 * inv, num1 * inv);
-    }
-    consumer_bar();   // the next item rewrites sQ and the merge buffers
   }
 }
 
@@ -860,6 +628,28 @@ __global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G
   if (threadIdx.x == 0) work[n_seq] = carry;
 }
 
+// tcgen05 attention (hm_attn_tc.cu), opt-in with HM_ATTN_TC=1 while its decode throughput is below the
+// mma.sync kernels' (it needs a work list and the cache geometry for the TMA maps); both families are
+// batch invariant, but a run must not mix them (speculative and greedy rows must share one kernel family)
+constexpr int kTcRows = 128;
+template <int HD>
+int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
+                   const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
+                   void* d_out, const int32_t* d_work, const CUtensorMap& mk, const CUtensorMap& mv,
+                   cudaStream_t st);
+inline bool attn_tc_enabled() {
+  static const bool on = getenv("HM_ATTN_TC") != nullptr && getenv("HM_ATTN_V2") == nullptr;
+  return on;
+}
+
+// exact work skips of k_attention2 (bit 0: rescale only when a row max moved, bit 1: skip slices
+// of padding rows, bit 2: unmasked fast path for fully visible key blocks); HM_ATTN_FLAGS overrides
+// the default (all on) for A/B profiling only
+inline int attn_flags() {
+  static const int f = getenv("HM_ATTN_FLAGS") ? atoi(getenv("HM_ATTN_FLAGS")) : 7;
+  return f;
+}
+
 template <int HD, int SL>
 int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
@@ -897,30 +687,16 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
       k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
       hm_count_launches(1);
     }
-    static const bool no_v3 = getenv("HM_ATTN_NO_V3") != nullptr;   // A/B switch for profiling only
-    if (SL == 2 && use_tma && !no_v3) {
-      // warp-specialised verify kernel: 4-stage ring + separate merge buffers, one CTA per SM
-      const int smem3 = 2 * 4 * 64 * HD * 2 + ROWS * HD * 2 + 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4 + 1024;
-      static bool set3 = false;
-      if (!set3) {
-        cudaFuncSetAttribute(k_attention3<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-        set3 = true;
-      }
-      k_attention3<HD><<<n_sm, 288, smem3, st>>>((const __nv_bfloat16*)d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, H,
-                                                 KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work, mk,
-                                                 mv);
-      return 0;
-    }
     k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
         d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
-        mk, mv, use_tma);
+        mk, mv, use_tma, attn_flags());
   } else {
     dim3 grid(KVH, n_seq);
     k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                   (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
                                                   d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
-                                                  (__nv_bfloat16*)d_out, n_seq, nullptr, mk, mv, use_tma);
+                                                  (__nv_bfloat16*)d_out, n_seq, nullptr, mk, mv, use_tma, attn_flags());
   }
   return 0;
 }
@@ -934,7 +710,8 @@ extern "C" int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t 
   if (n_seq <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
   const int G = H / KVH;
-  const int rows = max_q_len * G <= 16 ? 16 : 32;   // must match the tile height chosen in hm_attention
+  // must match the tile height chosen in hm_attention (which re-plans if it cannot take the tcgen05 path)
+  const int rows = hm::attn_tc_enabled() ? hm::kTcRows : (max_q_len * G <= 16 ? 16 : 32);
   hm::k_attn_tiles<<<1, 1024, 0, (cudaStream_t)stream>>>(d_q_len, n_seq, G, rows, d_work);
   hm_count_launches(1);
   cudaError_t e = cudaGetLastError();
@@ -953,6 +730,29 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
   dim3 grid((max_q_len * G + hm::AT_ROWS - 1) / hm::AT_ROWS, KVH, n_seq);
   const float scale_log2 = scale * 1.4426950408889634f;
   cudaStream_t st = (cudaStream_t)stream;
+  if (hm::attn_tc_enabled()) {
+    // tcgen05 path: needs the persistent work list and the cache geometry for the TMA maps
+    CUtensorMap mk, mv;
+    const int64_t rows = (int64_t)n_slots * KVH * max_len;
+    if (d_work && n_slots > 0 && (hd == 128 || hd == 64) && hm_make_tma_map(&mk, d_kcache, rows, hd, hd, 64) &&
+        hm_make_tma_map(&mv, d_vcache, rows, hd, hd, 64)) {
+      if (!work_ready) {
+        hm::k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, hm::kTcRows, d_work);
+        hm_count_launches(1);
+      }
+      if (hd == 128)
+        hm::launch_attn_tc<128>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
+                                d_work, mk, mv, st);
+      else
+        hm::launch_attn_tc<64>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
+                               d_work, mk, mv, st);
+      hm_count_launches(1);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }
+      return HM_OK;
+    }
+    work_ready = 0;   // a plan made for the tensor-core tiles does not fit the fallback's tile height
+  }
   const bool v1 = getenv("HM_ATTN_V1") != nullptr;   // A/B switch for profiling only
   if (!v1 && (hd == 128 || hd == 64)) {
     // rows per CTA tile: 16 when a whole (sequence, kv head) block fits, else 32

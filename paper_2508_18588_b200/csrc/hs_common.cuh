@@ -41,8 +41,11 @@ struct PowTable {
 };
 static __constant__ PowTable kPow = PowTable();
 
+// Linear in (slot, m): the final mix64 of gram_hash does the avalanche.  Hash
+// collisions only lengthen probe sequences -- a lookup accepts an entry after
+// the slot-range check and a text comparison, never on the hash alone.
 __host__ __device__ __forceinline__ uint64_t gram_seed(int32_t slot, int32_t m) {
-  return mix64(((uint64_t)(uint32_t)slot << 8) ^ (uint64_t)m ^ 0x5bd1e9955bd1e995ULL);
+  return (uint64_t)((uint32_t)slot + 1u) * 0xD6E8FEB86659FD93ULL + (uint64_t)(uint32_t)m * 0xA0761D6478BD642FULL;
 }
 __device__ __forceinline__ uint64_t gram_term(int32_t tok, int j) {
   return (uint64_t)((uint32_t)tok + 1u) * kPow.v[j];

@@ -42,6 +42,7 @@ class RolloutResult:
     tokens_per_iter: list = field(default_factory=list)
     flops: float = 0.0
     kv_bytes: float = 0.0
+    qlen_hist: np.ndarray = None  # [1 + max_q] count of (sequence, iteration) verify blocks by rows
 
     @property
     def generated(self) -> int:
@@ -142,6 +143,8 @@ class RolloutEngine:
         acc[2] = B * P * (P + 1) // 2
         acc[3] = B * P
         row_ids = torch.arange(self.fwd.max_rows, dtype=torch.int32, device=self.device)
+        qhist = torch.zeros(self.max_q + 1, dtype=torch.int64, device=self.device)
+        ones = torch.ones(B, dtype=torch.int64, device=self.device)
         R = min(self.fwd.max_rows, B * self.max_q)
 
         def iteration():
@@ -161,6 +164,7 @@ class RolloutEngine:
             acc[1] += (m > 0).to(torch.int64)
             acc[2] += torch.where(live, self.pos[:R].to(torch.int64) + 1, 0).sum()
             acc[3] += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
+            qhist.index_add_(0, self.q_len[:B].to(torch.int64), ones)
             am = self.fwd.run(R, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
                               self.kv_slot, B, self.max_q, stream=s, m_dev=self.d_m)
             state.accept_greedy(am, self.q_off, s)
@@ -198,8 +202,10 @@ class RolloutEngine:
         flops = (2.0 * (cfg.body_params() + cfg.vocab * cfg.d_model) * rows
                  + 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * float(a[2]))
         kv_bytes = float(cfg.kv_bytes_per_token) * float(a[3])
+        qh = qhist.cpu().numpy()
+        qh[0] = 0   # finished sequences
         res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms, flops=flops,
-                            kv_bytes=kv_bytes)
+                            kv_bytes=kv_bytes, qlen_hist=qh)
         per = max(1, self.prefill_rows // P)
         res.forwards = (iters - 1) + (B + per - 1) // per   # decode/verify forwards + prefill chunks
         res.weight_bytes = float(self.w.nbytes())
@@ -208,26 +214,30 @@ class RolloutEngine:
         return res
 
 
-def profile_forward(engine: RolloutEngine, B: int, ctx: int, q: int):
-    """One verify forward of B sequences x q rows at context `ctx`, each launch bracketed by CUDA events.
+def profile_forward(engine: RolloutEngine, B: int, ctx: int, q):
+    """One verify forward of B sequences at context `ctx`, each launch bracketed by CUDA events.
 
+    q: rows per sequence -- an int, or a length-B array of per-sequence verify
+    block sizes (e.g. sampled from RolloutResult.qlen_hist).
     Returns ({label: (total_ms, launches)}, M).  Used by bench.py for the
     per-kernel roofline (times measured live, not under a profiler).
     """
     import torch
     dev = engine.device
-    M = B * q
+    ql = np.full(B, int(q), np.int32) if np.isscalar(q) else np.asarray(q, dtype=np.int32)
+    M = int(ql.sum())
+    qmax = int(ql.max())
     i32 = dict(dtype=torch.int32, device=dev)
     tokens = torch.randint(0, engine.cfg.vocab, (M,), **i32)
-    pos = (torch.arange(q, **i32).repeat(B) + ctx)
-    row_slot = torch.arange(B, **i32).repeat_interleave(q)
-    q_off = torch.arange(B, **i32) * q
-    q_len = torch.full((B,), q, **i32)
+    q_len = torch.as_tensor(ql).to(dev)
+    q_off = torch.as_tensor(np.concatenate([[0], np.cumsum(ql)[:-1]]).astype(np.int32)).to(dev)
+    row_slot = torch.arange(B, **i32).repeat_interleave(q_len)
+    pos = torch.arange(M, **i32) - q_off.repeat_interleave(q_len) + ctx
     pos0 = torch.full((B,), ctx, **i32)
     kv = torch.arange(B, **i32)
-    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, q)   # warm
+    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qmax)   # warm
     prof = []
-    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, q, prof=prof)
+    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qmax, prof=prof)
     torch.cuda.synchronize(dev)
     out = {}
     for label, e0, e1 in prof:

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--q", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--skip-lookup", action="store_true")
+    ap.add_argument("--qhist-json", default=None,
+                    help="bench.py JSON line: sample per-sequence verify rows from its verify_rows_hist")
     args = ap.parse_args()
     import torch
     from paper_2508_18588_b200.engine import RolloutEngine, profile_forward
@@ -28,7 +30,13 @@ def main():
     torch.cuda.set_device(0)
     w = Weights(QWEN25_1P5B, "cuda", seed=0)
     eng = RolloutEngine(QWEN25_1P5B, w, n_slots=args.batch, max_len=args.ctx + 64, device="cuda")
-    prof, M = profile_forward(eng, args.batch, args.ctx, args.q)
+    q = args.q
+    if args.qhist_json:
+        h = json.load(open(args.qhist_json))["verify_rows_hist"]
+        vals = np.array([int(k) for k in h], dtype=np.int32)
+        cnt = np.array([h[k] for k in h], dtype=np.float64)
+        q = np.random.default_rng(77).choice(vals, size=args.batch, p=cnt / cnt.sum())
+    prof, M = profile_forward(eng, args.batch, args.ctx, q)
     print(json.dumps({"M": M, "ctx": args.ctx, "kernels": {k: v[0] for k, v in prof.items()}}))
     if not args.skip_lookup:
         import ctypes
