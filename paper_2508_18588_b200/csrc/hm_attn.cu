@@ -632,6 +632,7 @@ __global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G
 // mma.sync kernels' (it needs a work list and the cache geometry for the TMA maps); both families are
 // batch invariant, but a run must not mix them (speculative and greedy rows must share one kernel family)
 constexpr int kTcRows = 128;
+constexpr int kTcKeys = 128;   // keys per K/V stage: the TMA box height of the tcgen05 path
 template <int HD>
 int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                    const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
@@ -734,8 +735,9 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     // tcgen05 path: needs the persistent work list and the cache geometry for the TMA maps
     CUtensorMap mk, mv;
     const int64_t rows = (int64_t)n_slots * KVH * max_len;
-    if (d_work && n_slots > 0 && (hd == 128 || hd == 64) && hm_make_tma_map(&mk, d_kcache, rows, hd, hd, 64) &&
-        hm_make_tma_map(&mv, d_vcache, rows, hd, hd, 64)) {
+    if (d_work && n_slots > 0 && (hd == 128 || hd == 64) &&
+        hm_make_tma_map(&mk, d_kcache, rows, hd, hd, hm::kTcKeys) &&
+        hm_make_tma_map(&mv, d_vcache, rows, hd, hd, hm::kTcKeys)) {
       if (!work_ready) {
         hm::k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, hm::kTcRows, d_work);
         hm_count_launches(1);

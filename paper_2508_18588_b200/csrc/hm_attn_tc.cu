@@ -6,24 +6,29 @@
 // Work item = (sequence, kv head, 128-row tile) from the persistent work list
 // (hm_attention_plan); its rows are the (query i, head j of the GQA group)
 // pairs, so a verify block of up to 21 queries (GQA-6) is one item and its
-// KV stream is read from HBM once.  One CTA per SM:
-//   warp 0   TMA producer: K and V stages (64 keys) into separate 4-deep
+// KV stream is read from HBM once.  One CTA per SM, 10 warps:
+//   warp 0   TMA producer: K and V stages of 128 keys into separate 3-deep
 //            rings, K running ahead of V (K is released by S, V by P.V)
-//   warp 1   MMA issuer (one thread): S_j = Q K_j^T (M=128, N=64, K=hd) into
-//            a 3-deep TMEM S ring, up to three stages ahead of the softmax;
-//            O += P_j V_j (M=128, N=hd, K=64) with P read from its own
-//            double-buffered TMEM columns and V as an MN-major operand
-//   warps 2-5 softmax / correction / epilogue: thread = tile row = TMEM
-//            lane; a whole row of 64 scores per thread (no shuffles), P
-//            written to TMEM as packed bf16.  Warps whose 32 rows are all
-//            padding only keep the barrier cadence.
-// TMEM (512 columns): S ring [0, 192), P [192, 256), O [256, 256 + hd).
+//   warp 1   MMA issuer (one thread): S_j = Q K_j^T (M=128, N=128, K=hd, Q
+//            read from TMEM) into a 2-deep TMEM S ring; O += P_j V_j (M=128,
+//            N=hd, K=128) with P written by the softmax over the first half of
+//            S_j's columns and V as an MN-major operand.  Measured on B200
+//            (tools/dbg/umma_bench*.cu): an M=128 UMMA costs 45/64/128 cycles
+//            at N=64/128/256, so 128-key stages halve the issue cost per key.
+//   warps 2-9 softmax: two sets of four warps take alternate stages; in a
+//            set, warp w owns TMEM lane quarter w % 4 and reads it as two
+//            16-lane halves with tcgen05.ld.16x256b, so thread t holds rows
+//            t/4 and t/4 + 8 of the half and 32 of the stage's keys -- a
+//            decode block's few live rows get 4 threads each.  The packed P
+//            pairs are exactly the tcgen05.st.16x128b fragment.
 // Online softmax with a per-row lazy reference max: O and l are rescaled
 // only when a block max exceeds the reference by more than 8 (log2 units,
-// so P <= 256); the decision is per row, so every row's arithmetic depends
-// on its own query, position and the cache only -- a row computed in a
-// verify block is bit-identical to the same row decoded alone (greedy under
-// speculation stays bit-exact with greedy decoding).
+// so P <= 256); the reference passes between the sets through shared
+// memory.  Every decision is per row, so a row's arithmetic depends only on
+// its own query, position and the cache -- a row computed in a verify block
+// is bit-identical to the same row decoded alone (greedy under speculation
+// stays bit-exact with greedy decoding).
+
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <cstdio>
@@ -40,19 +45,15 @@ namespace hm {
 template <int HD>
 struct TcAttn {
   static constexpr int ROWS = 128;                    // UMMA M: tile rows
-  static constexpr int KS = 64;                       // keys per stage (UMMA N of S, K of P.V)
-  static constexpr int NSK = 4, NSV = 4;              // K / V smem ring depths
-  static constexpr int NS = 3, NP = 2;                // TMEM S ring / P buffers
+  static constexpr int KS = 128;                      // keys per stage (UMMA N of S, K of P.V)
+  static constexpr int NSK = 2, NSV = 3;              // K / V smem ring depths
+  static constexpr int NS = 3;                        // TMEM S ring (P aliases the first KS/2 columns)
   static constexpr int QB = ROWS * HD * 2;            // Q tile: [HD/64][ROWS][128 B], 128B-swizzled
   static constexpr int KVB = KS * HD * 2;             // one K or V stage: [HD/64][KS][128 B]
-  // V slot: the stage's HD/64 column groups plus a constant group whose first column is 1.0, so
-  // P.V with N = HD + 16 also accumulates the row sum l = sum_k P[k] in O column HD
-  static constexpr int VSB = KVB + KS * 128;
-  static constexpr int NO = HD + 16;                  // UMMA N of P.V
-  static constexpr int SMEM = QB + NSK * KVB + NSV * VSB + 1024;   // QB: the next item's Q, staged
+  static constexpr int SMEM = 2 * QB + (NSK + NSV) * KVB + 1024;   // Q double-buffered across items
   static constexpr int TMEM_COLS = 512;
-  // S ring [0, 192), P [192, 256), O and l [256, 256 + HD + 16) (+16 spare), Q (bf16 pairs) [448, 448 + HD/2)
-  static constexpr uint32_t COL_S = 0, COL_P = 192, COL_O = 256, COL_Q = 448;
+  // S ring [0, 384) (P = packed bf16 pairs over the first KS/2 columns of its S buffer), O [384, 384 + HD)
+  static constexpr uint32_t COL_S = 0, COL_O = 384;
 };
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -76,6 +77,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+// 16x256b.x16: 16 lanes x 128 columns (r[4i + 0/1] = (a, 8i + 2q + 0/1), r[4i + 2/3] = (b, ...))
+__device__ __forceinline__ void tmem_ld_16x256b_x16(uint32_t taddr, uint32_t* r) {
+  tmem_ld_16x256b_x8(taddr, r);
+  tmem_ld_16x256b_x8(taddr + 64, r + 32);
+}
+// 16x128b.x16: 16 lanes x 64 columns (r[2i] = (a, 4i + q), r[2i + 1] = (b, 4i + q))
+__device__ __forceinline__ void tmem_st_16x128b_x16(uint32_t taddr, const uint32_t* r) {
+  tmem_st_16x128b_x8(taddr, r);
+  tmem_st_16x128b_x8(taddr + 32, r + 16);
 }
 
 #ifdef HM_TC_WATCHDOG
@@ -112,25 +123,18 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
                                                     const __grid_constant__ CUtensorMap tmK,
                                                     const __grid_constant__ CUtensorMap tmV) {
   using C = TcAttn<HD>;
-  constexpr int ROWS = C::ROWS, KS = C::KS, NSK = C::NSK, NSV = C::NSV, NS = C::NS, NP = C::NP;
+  constexpr int ROWS = C::ROWS, KS = C::KS, NSK = C::NSK, NSV = C::NSV, NS = C::NS;
   const int G = H / KVH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sm + C::QB;              // [NSK][KVB] (after the Q staging buffer)
-  uint8_t* sV = sK + NSK * C::KVB;       // [NSV][VSB]
-  // the constant "ones" group of every V slot: key row k, element 0 = 1.0 (128B-swizzled like TMA writes)
-  for (int i = threadIdx.x; i < NSV * KS * 8; i += blockDim.x) {
-    const int slot = i / (KS * 8), k = (i / 8) % KS, chunk = i % 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if ((chunk ^ (k & 7)) == 0) v.x = 0x3F80u;   // bf16 1.0 in the low half: element 0 of the row
-    *reinterpret_cast<uint4*>(sV + slot * C::VSB + C::KVB + k * 128 + chunk * 16) = v;
-  }
-  fence_proxy_async_smem();
+  uint8_t* sQ = sm;                      // [2][QB]: Q tiles by item parity
+  uint8_t* sK = sm + 2 * C::QB;          // [NSK][KVB]
+  uint8_t* sV = sK + NSK * C::KVB;       // [NSV][KVB]
   __shared__ uint64_t k_full[NSK], k_empty[NSK], v_full[NSV], v_empty[NSV];
-  __shared__ uint64_t s_full[NS], s_free[NS], p_full[NP], p_free[NP], o_ready, q_full[2], o_free, m_ready[2];
-  __shared__ float m_sh[ROWS];   // per-row lazy reference max after the latest stage (handed between the sets)
+  __shared__ uint64_t s_full[NS], p_full[NS], p_done[NS], o_ready, q_full[2], o_free, m_ready[2], l_ready[2];
+  __shared__ float m_sh[ROWS];       // per-row lazy reference max after the latest stage (handed between the sets)
+  __shared__ float l_sh[2 * ROWS];   // per-row sum of P, gathered for the epilogue (by item parity)
   __shared__ uint32_t tmem_base;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSK; ++i) {
@@ -143,18 +147,16 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     }
     for (int i = 0; i < NS; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-    }
-    for (int i = 0; i < NP; ++i) {
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_free[i], 1);
+      mbar_init(&p_done[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&m_ready[i], 4);
+      mbar_init(&l_ready[i], 4);
+      mbar_init(&q_full[i], 4);
     }
     mbar_init(&o_ready, 1);
-    mbar_init(&q_full[0], 4);
-    mbar_init(&q_full[1], 4);
     mbar_init(&o_free, 4);
-    mbar_init(&m_ready[0], 4);
-    mbar_init(&m_ready[1], 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&tmem_base);
@@ -221,41 +223,43 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
             mbar_arrive_expect_tx(&v_full[slot], C::KVB);
 #pragma unroll
             for (int hb = 0; hb < HD / 64; ++hb)
-              tma_load_2d(&tmV, &v_full[slot], sV + slot * C::VSB + hb * KS * 128, hb * 64, cv.row0 + cv.st * KS);
+              tma_load_2d(&tmV, &v_full[slot], sV + slot * C::KVB + hb * KS * 128, hb * 64, cv.row0 + cv.st * KS);
             ++cv.st;
             ++cv.g;
             vmore = advance(cv);
           }
         }
-        if (ck.g + cv.g == issued) __nanosleep(64);   // both rings full: back off (shares an SMSP with a softmax warp)
+        if (ck.g + cv.g == issued) __nanosleep(64);   // both rings full: back off (shares an SMSP with softmax warps)
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
     if (lane == 0) {
-      const uint32_t id_s = idesc_bf16(ROWS, KS);                     // Q, K both K-major
-      const uint32_t id_pv = idesc_bf16(ROWS, C::NO) | (1u << 16);    // [V | ones]: MN-major B operand
-      uint32_t g = 0, items = 0;
-      uint64_t kdesc[NSK], vdesc[NSV];   // base smem descriptors of the K and V ring slots
+      const uint32_t id_s = idesc_bf16(ROWS, KS);                     // A = Q, B = K (both K-major smem)
+      const uint32_t id_pv = idesc_bf16(ROWS, HD) | (1u << 16);       // A = P (TMEM), B = V (MN-major smem)
+      uint64_t kdesc[NSK], vdesc[NSV], qdesc[2];   // base descriptors (per-step offsets are constants)
 #pragma unroll
       for (int i = 0; i < NSK; ++i) kdesc[i] = smem_desc_sw128(sK + i * C::KVB);
 #pragma unroll
-      for (int i = 0; i < NSV; ++i) vdesc[i] = smem_desc_sw128_mn(sV + i * C::VSB, KS * 128);
+      for (int i = 0; i < NSV; ++i) vdesc[i] = smem_desc_sw128_mn(sV + i * C::KVB, KS * 128);
+      qdesc[0] = smem_desc_sw128(sQ);
+      qdesc[1] = smem_desc_sw128(sQ + C::QB);
+      uint32_t g = 0, items = 0;
       auto issue_s = [&](uint32_t gs) {
         const int slot = gs % NSK, b = gs % NS;
         MBAR_WAIT(&k_full[slot], (gs / NSK) & 1, 1, gs);
         TC_TRACE(4, gs);
-        if (gs >= (uint32_t)NS) MBAR_WAIT(&s_free[b], ((gs / NS) - 1) & 1, 2, gs);   // softmax has read S_{gs-NS}
+        // S buffer b last held S_{gs-NS} and P_{gs-NS}: wait until P_{gs-NS}.V_{gs-NS} has read it
+        if (gs >= (uint32_t)NS) MBAR_WAIT(&p_done[b], ((gs / NS) - 1) & 1, 2, gs);
         tc_fence_after();
-        // A = Q from TMEM (16 elements = 8 packed columns per K step): only K is read from smem.  The K
-        // descriptors differ from the slot's base descriptor by constant start-address offsets (16-byte
-        // units), so each issue is one add -- rebuilding a descriptor per MMA costs more than the MMA.
-        const uint64_t kd0 = kdesc[slot];
-        const uint32_t d_s = tbase + C::COL_S + b * KS, a_q = tbase + C::COL_Q;
+        const uint64_t kd0 = kdesc[slot], qd0 = qdesc[items & 1];
+        const uint32_t d_s = tbase + C::COL_S + b * KS;
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          umma_f16_ts(d_s, a_q + kk * 8, kd0 + (uint64_t)(((kk >> 2) * KS * 128 + (kk & 3) * 32) >> 4), id_s,
-                      kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off_q = ((kk >> 2) * ROWS * 128 + (kk & 3) * 32) >> 4;
+          const uint32_t off_k = ((kk >> 2) * KS * 128 + (kk & 3) * 32) >> 4;
+          umma_f16(d_s, qd0 + off_q, kd0 + off_k, id_s, kk > 0 ? 1u : 0u);
+        }
         umma_commit(&k_empty[slot]);
         umma_commit(&s_full[b]);
         TC_TRACE(0, gs);
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
       int n_stage = (int)blockIdx.x < n_items ? stages_of(blockIdx.x) : 0;
       for (int it = blockIdx.x; it < n_items; ++items) {
         const int it_next = it + gridDim.x;
-        MBAR_WAIT(&q_full[0], items & 1, 3, (int)g);   // this item's Q is in TMEM
+        MBAR_WAIT(&q_full[items & 1], (items >> 1) & 1, 3, (int)g);   // this item's Q tile is in smem
         tc_fence_after();
         for (int i = 0; i < NS && i < n_stage; ++i) issue_s(g + i);
         const int n_next = it_next < n_items ? stages_of(it_next) : 0;   // its loads overlap the S MMAs
@@ -278,19 +282,19 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
         }
         for (int st = 0; st < n_stage; ++st) {
           const uint32_t gs = g + st;
-          const int vslot = gs % NSV, pb = gs & 1;
-          MBAR_WAIT(&p_full[pb], (gs >> 1) & 1, 5, gs);
+          const int vslot = gs % NSV, b = gs % NS;
+          MBAR_WAIT(&p_full[b], (gs / NS) & 1, 5, gs);
           TC_TRACE(1, gs);
           MBAR_WAIT(&v_full[vslot], (gs / NSV) & 1, 6, gs);
           TC_TRACE(5, gs);
           tc_fence_after();
           const uint64_t vd0 = vdesc[vslot];
-          const uint32_t a_p = tbase + C::COL_P + pb * 32, d_o = tbase + C::COL_O;
+          const uint32_t a_p = tbase + C::COL_S + b * KS, d_o = tbase + C::COL_O;
 #pragma unroll
           for (int kk = 0; kk < KS / 16; ++kk)   // 16 keys = 2 K groups of 8 rows x 128 B per step
             umma_f16_ts(d_o, a_p + kk * 8, vd0 + (uint64_t)(kk * 2048 >> 4), id_pv, (st > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&v_empty[vslot]);
-          umma_commit(&p_free[pb]);
+          umma_commit(&p_done[b]);
           if (st == n_stage - 1) umma_commit(&o_ready);   // the item's O is complete
           if (st + NS < n_stage) issue_s(gs + NS);
         }
@@ -300,15 +304,19 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
       }
     }
   } else {
-    // ---------------- softmax / correction / epilogue: thread = tile row = TMEM lane
-    // TMEM lane (= UMMA row = Q smem row) tl; tile row (tl + 64) mod 128, so the first 64 tile rows --
-    // all of a decode or short verify block -- sit on warps 2 and 3, whose SM sub-partitions do not
-    // also host the producer and MMA warps
+    // ---------------- softmax / correction / epilogue
+    // TMEM lane (= UMMA row = Q row) tl; tile row (tl + 64) mod 128, so the first 64 tile rows -- all of a
+    // decode or short verify block -- sit on quarters 2 and 3, whose SM sub-partitions do not also host the
+    // producer and MMA warps.  Softmax fragment: half h of the quarter, thread t: lanes a = 16h + t/4 and
+    // b = a + 8 (of the quarter), keys 8i + 2q + {0,1}, q = t % 4.
     const int quarter = warp & 3;
-    const int set = (warp - 2) >> 2;   // softmax set: stages with (global stage & 1) == set
+    const int set = (warp - 2) >> 2;   // this set takes the stages with (global stage & 1) == set
     const int tl = quarter * 32 + lane;
     const int row = (tl + 64) & (ROWS - 1);
     const uint32_t t_lane = tbase + ((uint32_t)(quarter * 32) << 16);
+    const int q4 = lane & 3;
+    auto trow_of = [&](int h, int ab) { return (quarter * 32 + 16 * h + (lane >> 2) + 8 * ab + 64) & (ROWS - 1); };
+    auto lane_of = [&](int h, int ab) { return quarter * 32 + 16 * h + (lane >> 2) + 8 * ab; };
     struct Item {
       int s, kvh, tile, rows_total, rows_here, qo, p0, n_stage;
     };
@@ -322,186 +330,214 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
       x.n_stage = item_stages(x.s, x.tile);
       return x;
     };
-    // Q: this thread's row of an item is staged in smem early (global latency off the critical path),
-    // then moved into the TMEM Q columns -- one packed bf16 pair per column -- once the previous
-    // item's products are done, and handed to the MMA warp on q_full (zeros for padding rows)
-    auto stage_q = [&](const Item& x) {
+    // Q: set 0 writes this thread's row of an item into the item's smem Q tile (128B-swizzled, K-major:
+    // the S products' A operand) and hands it over on q_full[buffer]; zeros for padding rows
+    auto write_q = [&](const Item& x, int qbuf) {
       const bool lv = row < x.rows_here;
       const int r2 = x.tile * ROWS + row;
       const uint4* src = reinterpret_cast<const uint4*>(
           q + ((size_t)(x.qo + (lv ? r2 / G : 0)) * H + x.kvh * G + (lv ? r2 % G : 0)) * HD);
+      uint8_t* dq = sQ + qbuf * C::QB;
 #pragma unroll
       for (int ch = 0; ch < HD / 8; ++ch) {
         const uint4 v = lv ? src[ch] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sQ + (ch >> 3) * ROWS * 128 + tl * 128 + (((ch & 7) ^ (tl & 7)) << 4)) = v;
+        *reinterpret_cast<uint4*>(dq + (ch >> 3) * ROWS * 128 + tl * 128 + (((ch & 7) ^ (tl & 7)) << 4)) = v;
       }
-    };
-    auto commit_q = [&]() {
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        uint32_t w[32];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sQ + c * ROWS * 128 + tl * 128 + ((k ^ (tl & 7)) << 4));
-          w[4 * k + 0] = v.x;
-          w[4 * k + 1] = v.y;
-          w[4 * k + 2] = v.z;
-          w[4 * k + 3] = v.w;
-        }
-        tmem_st32(t_lane + C::COL_Q + c * 32, w);
-      }
-      tmem_wait_st();
-      tc_fence_before();
+      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&q_full[0]);
+      if (lane == 0) mbar_arrive(&q_full[qbuf]);
     };
     uint32_t g = 0, items = 0;
     Item cur;
     if ((int)blockIdx.x < n_items) {
       cur = item_info(blockIdx.x);
-      if (set == 0) {
-        stage_q(cur);
-        commit_q();
-      }
+      if (set == 0) write_q(cur, 0);
     }
     for (int it = blockIdx.x; it < n_items; ++items) {
+      // the next item's Q goes into the other buffer now, so the MMA warp can start its S products while
+      // this item's epilogue runs (that buffer was last read by the previous item's S products, all done)
       const int it_next = it + gridDim.x;
       Item nxt;
       if (it_next < n_items) {
         nxt = item_info(it_next);
-        if (set == 0) stage_q(nxt);   // this thread re-reads only its own staged row: no barrier needed
+        if (set == 0) write_q(nxt, (items + 1) & 1);
       }
-      const int kvh = cur.kvh, tile = cur.tile, rows_here = cur.rows_here;
-      const int qo = cur.qo, p0 = cur.p0, n_stage = cur.n_stage;
-      const bool live = row < rows_here;
-      const bool warp_live = ((tl - lane + 64) & (ROWS - 1)) < rows_here;   // warp-uniform
-      const int rr = tile * ROWS + row;
-      const int rpos = live ? p0 + rr / G : -1;          // -1: padding row, fully masked
-      // the two softmax sets take alternate stages; the per-row lazy reference max (log2 units) passes
-      // from one to the other through m_sh, ordered by m_ready (l accumulates in O column HD)
+      const int rows_here = cur.rows_here, n_stage = cur.n_stage;
+      int hpos[2][2];   // position of row (half, a/b); -1: padding row, fully masked
+      bool hlive[2];    // the half holds a live row (warp-uniform)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        hlive[h] = ((quarter * 32 + 16 * h + 64) & (ROWS - 1)) < rows_here;
+#pragma unroll
+        for (int ab = 0; ab < 2; ++ab) {
+          const int tr = trow_of(h, ab);
+          hpos[h][ab] = tr < rows_here ? cur.p0 + (cur.tile * ROWS + tr) / G : -1;
+        }
+      }
+      float lsum[2][2] = {{0.f, 0.f}, {0.f, 0.f}};   // this thread's part of each row's sum of P
       for (int st = 0; st < n_stage; ++st) {
         const uint32_t gs = g + st;
         if ((int)(gs & 1) != set) continue;
-        const int b = gs % NS, pb = gs & 1;
+        const int b = gs % NS;
+        const uint32_t t_s = t_lane + C::COL_S + b * KS;
         MBAR_WAIT(&s_full[b], (gs / NS) & 1, 7, gs);
-        if (warp_live && lane == 0) TC_TRACE(2, gs);
         tc_fence_after();
-        float sc[64];
-        if (warp_live) {
-          tmem_ld32(t_lane + C::COL_S + b * KS, sc);
-          tmem_ld32(t_lane + C::COL_S + b * KS + 32, sc + 32);
+        if (quarter == 2 && lane == 0) TC_TRACE(2, gs);
+        const int key0 = st * KS;
+        // the reference after stage gs-1 (the other set's); -inf at the item's first stage
+        if (gs >= 1) MBAR_WAIT(&m_ready[(gs - 1) & 1], ((gs - 1) >> 1) & 1, 12, gs);
+        float fac[2][2] = {{1.f, 1.f}, {1.f, 1.f}};
+        bool resc_any = false;
+        uint32_t pk[2][32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (!hlive[h]) continue;
+          uint32_t sv[64];
+          tmem_ld_16x256b_x16(t_s + ((uint32_t)(16 * h) << 16), sv);
+          tmem_wait_ld();
+          float* sc = reinterpret_cast<float*>(sv);   // sc[4i + 2ab + e]: row ab, key key0 + 8i + 2q + e
+          if (!__all_sync(0xffffffffu, key0 + KS - 1 <= hpos[h][0] && key0 + KS - 1 <= hpos[h][1])) {
+#pragma unroll
+            for (int ab = 0; ab < 2; ++ab) {
+              const int nv = hpos[h][ab] - key0;   // keys key0 + k, k <= nv, are visible to the row
+#pragma unroll
+              for (int i = 0; i < KS / 8; ++i)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                  if (8 * i + 2 * q4 + e > nv) sc[4 * i + 2 * ab + e] = -INFINITY;
+            }
+          }
+#pragma unroll
+          for (int ab = 0; ab < 2; ++ab) {
+            // raw-score row max over the 4 threads of the row; the log2-domain scale is folded into the
+            // exponent's fma (scale > 0: the max of the scaled scores is the scaled max, exactly)
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < KS / 8; ++i) {
+              mx0 = fmaxf(mx0, sc[4 * i + 2 * ab]);
+              mx1 = fmaxf(mx1, sc[4 * i + 2 * ab + 1]);
+            }
+            float mx = fmaxf(mx0, mx1);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float bmax = mx * scale_log2;
+            const int ln = lane_of(h, ab);
+            const float m_ref = st > 0 ? m_sh[ln] : -INFINITY;
+            float m_new = m_ref;
+            if (bmax > -INFINITY) {
+              if (m_ref == -INFINITY) {
+                m_new = bmax;   // first visible block: O and l are still 0
+              } else if (bmax > m_ref + 8.f) {
+                m_new = bmax;
+                fac[h][ab] = ex2f(m_ref - m_new);
+                resc_any = true;
+              }
+            }
+            if (q4 == 0) m_sh[ln] = m_new;
+            const float sub = m_new == -INFINITY ? 0.f : m_new;
+            float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < KS / 8; ++i) {
+              const float p0 = ex2f(fmaf(sc[4 * i + 2 * ab], scale_log2, -sub));
+              const float p1 = ex2f(fmaf(sc[4 * i + 2 * ab + 1], scale_log2, -sub));
+              ls0 += p0;
+              ls1 += p1;
+              pk[h][2 * i + ab] = pack2(p0, p1);
+            }
+            lsum[h][ab] = fmaf(lsum[h][ab], fac[h][ab], ls0 + ls1);
+          }
         }
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[b]);   // S_gs is in registers: the MMA may refill the buffer
-        if (warp_live) {
-          const int key0 = st * KS;
-          float mx[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-          // raw scores; the log2-domain scale is folded into the exponent's fma (scale > 0, so the
-          // block max of the scaled scores is the scaled max, exactly)
-          if (__all_sync(0xffffffffu, !live || key0 + KS - 1 <= rpos)) {   // no live row needs a mask
-#pragma unroll
-            for (int i = 0; i < 64; ++i) mx[i & 7] = fmaxf(mx[i & 7], sc[i]);
-          } else {
-            const int nv = rpos - key0;   // keys key0 + i, i <= nv, are visible to this row
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              sc[i] = i <= nv ? sc[i] : -INFINITY;
-              mx[i & 7] = fmaxf(mx[i & 7], sc[i]);
-            }
-          }
-          const float bmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                   fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * scale_log2;
-          // the reference after stage gs-1 (the other set's); -inf at the item's first stage
-          if (gs >= 1) MBAR_WAIT(&m_ready[(gs - 1) & 1], ((gs - 1) >> 1) & 1, 12, gs);
-          const float m_ref = st > 0 ? m_sh[tl] : -INFINITY;
-          float m_new = m_ref;
-          bool resc = false;
-          if (bmax > -INFINITY) {
-            if (m_ref == -INFINITY) {
-              m_new = bmax;   // first visible block: O and l are still 0
-            } else if (bmax > m_ref + 8.f) {
-              m_new = bmax;
-              resc = true;
-            }
-          }
-          m_sh[tl] = m_new;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&m_ready[gs & 1]);
-          if (__any_sync(0xffffffffu, resc)) {
-            // O holds P.V through stage gs-1 once P_{gs-1}.V_{gs-1} is done; scale this warp's rows
-            // (factor 1 for the others: an exact no-op)
-            MBAR_WAIT(&p_free[(gs - 1) & 1], ((gs - 1) >> 1) & 1, 8, gs);
-            tc_fence_after();
-            const float f = resc ? ex2f(m_ref - m_new) : 1.f;
-#pragma unroll
-            for (int c = 0; c <= HD / 32; ++c) {   // O columns [0, HD) and l (column HD; 16 spare columns ride along)
-              float o[32];
-              tmem_ld32(t_lane + C::COL_O + c * 32, o);
-              uint32_t u[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(o[i] * f);
-              tmem_st32(t_lane + C::COL_O + c * 32, u);
-            }
-            tmem_wait_st();
-          }
-          const float sub = m_new == -INFINITY ? 0.f : m_new;
-          uint32_t pk[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            pk[i] = pack2(ex2f(fmaf(sc[2 * i], scale_log2, -sub)), ex2f(fmaf(sc[2 * i + 1], scale_log2, -sub)));
-          // P buffer pb was last read by P_{gs-2}.V_{gs-2}
-          if (gs >= 2) MBAR_WAIT(&p_free[pb], ((gs >> 1) - 1) & 1, 9, gs);
+        if (lane == 0) mbar_arrive(&m_ready[gs & 1]);
+        if (__any_sync(0xffffffffu, resc_any)) {
+          // O holds P.V through stage gs-1 once P_{gs-1}.V_{gs-1} is done: scale the rows whose
+          // reference moved (factor 1 for the others: an exact no-op)
+          MBAR_WAIT(&p_done[(gs - 1) % NS], ((gs - 1) / NS) & 1, 8, gs);
           tc_fence_after();
-          tmem_st32(t_lane + C::COL_P + pb * 32, pk);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (!hlive[h]) continue;
+            const uint32_t t_o = t_lane + ((uint32_t)(16 * h) << 16) + C::COL_O;
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+              uint32_t o[32];
+              tmem_ld_16x256b_x8(t_o + c * 64, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * fac[h][(i >> 1) & 1]);
+              tmem_st_16x256b_x8(t_o + c * 64, o);
+            }
+          }
           tmem_wait_st();
-        } else {
-          // padding-only warps keep the cadence: an early arrival on m_ready or p_full for stage gs could
-          // land in the phase of stage gs-2 while a slower warp has not yet arrived for it
-          if (gs >= 1) MBAR_WAIT(&m_ready[(gs - 1) & 1], ((gs - 1) >> 1) & 1, 12, gs);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&m_ready[gs & 1]);
-          if (gs >= 2) MBAR_WAIT(&p_free[pb], ((gs >> 1) - 1) & 1, 11, gs);
         }
+        // P over the first KS/2 columns of S_gs (this set has read them; the MMA warp reads P next)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (hlive[h]) tmem_st_16x128b_x16(t_s + ((uint32_t)(16 * h) << 16), pk[h]);
+        tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[pb]);
-        if (warp_live && lane == 0) TC_TRACE(3, gs);
+        if (lane == 0) mbar_arrive(&p_full[b]);
+        if (quarter == 2 && lane == 0) TC_TRACE(3, gs);
       }
-      // epilogue (set 0): O / l for the live rows
-      if (set == 0) {
-      MBAR_WAIT(&o_ready, items & 1, 10, (int)g);
-      tc_fence_after();
-      // every product of this item is done: the next item's Q can replace this one in TMEM, and the MMA
-      // warp starts its S products while this epilogue reads O
-      if (it_next < n_items) commit_q();
-      if (warp_live) {
-        float lv[32];
-        tmem_ld32(t_lane + C::COL_O + HD, lv);   // l = sum of the bf16 P the tensor core accumulated
-        const float inv = lv[0] > 0.f ? 1.f / lv[0] : 0.f;
-        __nv_bfloat16* dst = out + ((size_t)(qo + (live ? rr / G : 0)) * H + kvh * G + (live ? rr % G : 0)) * HD;
+      // gather each row's sum of P (the 4 threads of a row, both sets) into l_sh
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          float o[32];
-          tmem_ld32(t_lane + C::COL_O + c * 32, o);
-          if (live) {
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 w;
-              w.x = pack2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
-              w.y = pack2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
-              w.z = pack2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
-              w.w = pack2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
-              *reinterpret_cast<uint4*>(dst + c * 32 + 8 * v) = w;
+        for (int ab = 0; ab < 2; ++ab) {
+          float v = lsum[h][ab];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          lsum[h][ab] = v;
+        }
+      float* lbuf = l_sh + (items & 1) * ROWS;   // per item parity: set 1 may run an item ahead of set 0
+      if (set == 1) {
+        // hand this set's sums of P over to set 0's epilogue
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ab = 0; ab < 2; ++ab)
+            if (q4 == 0) lbuf[lane_of(h, ab)] = lsum[h][ab];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&l_ready[items & 1]);
+      } else {
+        // epilogue (set 0), once every product of the item is done: O / l for the live rows
+        MBAR_WAIT(&o_ready, items & 1, 10, (int)g);
+        tc_fence_after();
+        MBAR_WAIT(&l_ready[items & 1], (items >> 1) & 1, 13, (int)g);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ab = 0; ab < 2; ++ab)
+            if (q4 == 0) lbuf[lane_of(h, ab)] += lsum[h][ab];
+        __syncwarp();
+        const bool live = row < rows_here;
+        if (((tl - lane + 64) & (ROWS - 1)) < rows_here) {   // the warp holds a live row
+          const float lrow = lbuf[tl];
+          const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
+          const int rr = cur.tile * ROWS + row;
+          __nv_bfloat16* dst =
+              out + ((size_t)(cur.qo + (live ? rr / G : 0)) * H + cur.kvh * G + (live ? rr % G : 0)) * HD;
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            float o[32];
+            tmem_ld32(t_lane + C::COL_O + c * 32, o);
+            if (live) {
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint4 w;
+                w.x = pack2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                w.y = pack2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                w.z = pack2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                w.w = pack2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                *reinterpret_cast<uint4*>(dst + c * 32 + 8 * v) = w;
+              }
             }
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_free);
       }
       g += n_stage;
       it = it_next;

@@ -391,8 +391,10 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
 
 extern "C" int hm_gemm_bn(int32_t n) {
   // tile width is a function of N only (batch invariance): 256 for wide N (a last tile may be half
-  // empty when N % 256 == 128, e.g. the 151,936-entry LM head), 128 otherwise
-  return (n >= 1536) ? 256 : 128;
+  // empty when N % 256 == 128, e.g. the 151,936-entry LM head), 128 otherwise.  N up to
+  // HM_GEMM_BN128_MAX also uses 128 (A/B of the wave quantisation of narrow GEMMs)
+  static const int bn128_max = getenv("HM_GEMM_BN128_MAX") ? atoi(getenv("HM_GEMM_BN128_MAX")) : 0;
+  return (n >= 1536 && n > bn128_max) ? 256 : 128;
 }
 
 static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
@@ -428,7 +430,20 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
     hm_set_error("hm_gemm: K must be a multiple of 64 and N of 128");
     return HM_ERR_INVALID;
   }
-  const int BN = hm_gemm_bn(N);
+  int BN = hm_gemm_bn(N);
+  // Plain and fp32 epilogues may narrow the tile when 256-wide tiles would leave SMs idle (decode-sized M):
+  // every output element's K reduction is the same sequence of K=16 MMA steps at either width, so a row's
+  // bits do not change (tests/test_model_gpu.py::test_gemm_tile_width_is_bit_neutral); SwiGLU's weight
+  // interleave and the argmax partials are laid out per hm_gemm_bn(N) and keep it.
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const int narrow_off = getenv("HM_GEMM_NO_NARROW") != nullptr;   // A/B switch for profiling only
+  if (BN == 256 && !narrow_off && (epi == HM_EPI_STORE || epi == HM_EPI_F32 || epi == HM_EPI_RESIDUAL) &&
+      ((M + hm::BM - 1) / hm::BM) * ((N + 255) / 256) < g_num_sms)
+    BN = 128;
   if (epi == HM_EPI_SWIGLU && N % BN != 0) {
     hm_set_error("hm_gemm: SwiGLU needs N to be a multiple of the tile width (interleave granularity)");
     return HM_ERR_INVALID;

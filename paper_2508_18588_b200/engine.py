@@ -145,7 +145,10 @@ class RolloutEngine:
         row_ids = torch.arange(self.fwd.max_rows, dtype=torch.int32, device=self.device)
         qhist = torch.zeros(self.max_q + 1, dtype=torch.int64, device=self.device)
         ones = torch.ones(B, dtype=torch.int64, device=self.device)
-        R = min(self.fwd.max_rows, B * self.max_q)
+        # launch geometry of the captured iteration: one row per sequence without speculation (decode-sized
+        # GEMM tiles and attention tiles), up to 1 + window rows per sequence with it
+        q_cap = self.max_q if spec_on else 1
+        R = min(self.fwd.max_rows, B * q_cap)
 
         def iteration():
             # one engine iteration, fully device-driven (row count lives in d_m): graph-capturable
@@ -166,7 +169,7 @@ class RolloutEngine:
             acc[3] += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
             qhist.index_add_(0, self.q_len[:B].to(torch.int64), ones)
             am = self.fwd.run(R, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
-                              self.kv_slot, B, self.max_q, stream=s, m_dev=self.d_m)
+                              self.kv_slot, B, q_cap, stream=s, m_dev=self.d_m)
             state.accept_greedy(am, self.q_off, s)
 
         # first decode iteration eagerly (initializes kernel attributes), then replay a captured graph
@@ -214,11 +217,13 @@ class RolloutEngine:
         return res
 
 
-def profile_forward(engine: RolloutEngine, B: int, ctx: int, q):
+def profile_forward(engine: RolloutEngine, B: int, ctx: int, q, launch_rows=None, launch_q=None):
     """One verify forward of B sequences at context `ctx`, each launch bracketed by CUDA events.
 
     q: rows per sequence -- an int, or a length-B array of per-sequence verify
     block sizes (e.g. sampled from RolloutResult.qlen_hist).
+    launch_rows / launch_q: launch geometry as the engine's captured iteration uses it (rows sized for
+    the worst case, live count on the device; max rows per sequence); default: the exact sizes.
     Returns ({label: (total_ms, launches)}, M).  Used by bench.py for the
     per-kernel roofline (times measured live, not under a profiler).
     """
@@ -235,9 +240,17 @@ def profile_forward(engine: RolloutEngine, B: int, ctx: int, q):
     pos = torch.arange(M, **i32) - q_off.repeat_interleave(q_len) + ctx
     pos0 = torch.full((B,), ctx, **i32)
     kv = torch.arange(B, **i32)
-    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qmax)   # warm
+    R, qcap, m_dev = M, qmax, None
+    if launch_rows is not None:
+        R, qcap = max(launch_rows, M), max(launch_q or qmax, qmax)
+        pad = R - M
+        tokens = torch.cat([tokens, torch.zeros(pad, **i32)])
+        pos = torch.cat([pos, torch.zeros(pad, **i32)])
+        row_slot = torch.cat([row_slot, torch.zeros(pad, **i32)])
+        m_dev = torch.tensor([M], **i32)
+    engine.fwd.run(R, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qcap, m_dev=m_dev)   # warm
     prof = []
-    engine.fwd.run(M, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qmax, prof=prof)
+    engine.fwd.run(R, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qcap, m_dev=m_dev, prof=prof)
     torch.cuda.synchronize(dev)
     out = {}
     for label, e0, e1 in prof:

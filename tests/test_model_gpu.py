@@ -62,6 +62,29 @@ def test_gemm_rows_are_batch_invariant(torch):
         assert torch.equal(o, full[rows])
 
 
+@pytest.mark.parametrize("epi,N", [(0, 2048), (4, 1536)])
+def test_gemm_tile_width_is_bit_neutral(torch, epi, N):
+    """Decode-sized launches use 128-wide tiles, verify-sized ones 256-wide (N >= 1536): the rows they
+    share must be bit-identical (greedy under speculation stays bit-exact)."""
+    g = torch.Generator(device="cuda").manual_seed(N + epi)
+    K = 1536
+    x = torch.randn(3000, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16)
+
+    def run(M):   # M = 100: 1 x N/256 tiles < SMs -> 128-wide; M = 3000: 24 x N/256 >= SMs -> 256-wide
+        if epi == 0:
+            o = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+            _gemm(M, 0, x[:M].contiguous(), w, bias=b, out=o)
+        else:
+            o = torch.empty(M, N, dtype=torch.float32, device="cuda")
+            _gemm(M, 4, x[:M].contiguous(), w, resid=o)
+        return o
+
+    small, large = run(100), run(3000)
+    assert torch.equal(small, large[:100])
+
+
 def test_gemm_swiglu_residual_argmax(torch):
     from paper_2508_18588_b200.model import interleave_gate_up
     g = torch.Generator(device="cuda").manual_seed(5)

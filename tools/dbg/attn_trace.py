@@ -32,14 +32,14 @@ print("rc", f(ctypes.addressof(buf)))
 t = np.frombuffer(buf, dtype=np.int64).reshape(8, 512).astype(np.float64)
 t0 = t[0, 0]
 names = ["S issued", "p_full seen", "softmax S ready", "softmax P done", "K ready", "V ready"]
-for gs in list(range(0, 12)) + list(range(36, 44)) + list(range(200, 206)):
+for gs in list(range(0, 6)) + list(range(100, 106)):
     print(gs, " ".join("%s=%7.0f" % (names[e][:10], t[e, gs] - t0) for e in range(6)))
-d = np.diff(t[3, 40:400])
+d = np.diff(t[3, 40:200])
 print("softmax P-done period: median %.0f cycles" % np.median(d[d > 0]))
 for e in range(6):
-    x = np.diff(t[e, 40:400]); x = x[x > 0]
+    x = np.diff(t[e, 40:200]); x = x[x > 0]
     print(names[e], "period median", np.median(x))
-print("lag S-issued -> softmax ready (median)", np.median((t[2] - t[0])[40:400]))
-print("lag softmax ready -> P done (median)", np.median((t[3] - t[2])[40:400]))
-print("lag P done -> p_full seen by MMA (median)", np.median((t[1] - t[3])[40:400]))
-print("lag p_full seen -> V ready (median)", np.median((t[5] - t[1])[40:400]))
+print("lag S-issued -> softmax ready (median)", np.median((t[2] - t[0])[40:200]))
+print("lag softmax ready -> P done (median)", np.median((t[3] - t[2])[40:200]))
+print("lag P done -> p_full seen by MMA (median)", np.median((t[1] - t[3])[40:200]))
+print("lag p_full seen -> V ready (median)", np.median((t[5] - t[1])[40:200]))

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--q", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--skip-lookup", action="store_true")
+    ap.add_argument("--launch-rows", type=int, default=None, help="engine-style launch rows (live count on device)")
+    ap.add_argument("--launch-q", type=int, default=None, help="engine-style max rows per sequence")
     ap.add_argument("--qhist-json", default=None,
                     help="bench.py JSON line: sample per-sequence verify rows from its verify_rows_hist")
     args = ap.parse_args()
@@ -36,7 +38,7 @@ def main():
         vals = np.array([int(k) for k in h], dtype=np.int32)
         cnt = np.array([h[k] for k in h], dtype=np.float64)
         q = np.random.default_rng(77).choice(vals, size=args.batch, p=cnt / cnt.sum())
-    prof, M = profile_forward(eng, args.batch, args.ctx, q)
+    prof, M = profile_forward(eng, args.batch, args.ctx, q, launch_rows=args.launch_rows, launch_q=args.launch_q)
     print(json.dumps({"M": M, "ctx": args.ctx, "kernels": {k: v[0] for k, v in prof.items()}}))
     if not args.skip_lookup:
         import ctypes
