@@ -49,10 +49,12 @@ extern "C" {
 
 typedef void* hs_stream_t;    /* cudaStream_t */
 
+/* n-gram table entry.  The table buffer holds (table_mask + 1) entries followed by as many int64
+ * fixed-point reward masses (mass of entry i at ((int64_t*)(table + table_mask + 1))[i]): the draft
+ * hot path probes 8-byte entries and never touches the masses. */
 typedef struct {
   int32_t pos;    /* text position of the heavy occurrence; -1 = empty slot */
   int32_t tag;    /* hash bits | m */
-  int64_t mass;   /* fixed-point reward mass below the pattern */
 } HsGramEntry;
 
 typedef struct {

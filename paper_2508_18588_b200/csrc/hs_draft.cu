@@ -54,7 +54,8 @@ __device__ __forceinline__ Hit probe_table(const HsIndexView& V, int32_t slot, i
       if (!bad) {
         r.found = 1;
         r.pos = pos;
-        r.mass = __shfl_sync(0xffffffffu, e.mass, src);
+        // masses sit in a parallel array after the entries (the draft hot path never reads them)
+        r.mass = reinterpret_cast<const int64_t*>(V.table + (V.table_mask + 1))[(base + src) & V.table_mask];
         return r;
       }
       cands &= cands - 1;
@@ -355,6 +356,158 @@ __global__ void __launch_bounds__(256, 8) k_draft8(HsIndexView V, int32_t n_seq,
   }
 }
 
+// K2, 4-lane groups (default): eight sequences per warp, twice the queries in
+// flight of k_draft8 at the same occupancy -- the kernel is bound by its chain
+// of dependent loads (metadata -> prefix -> table row -> text), not by bytes.
+// Lane j of a group holds prefix tokens j and j + 4, probes table entries
+// base + 2j and base + 2j + 1 (8 entries of 8 B = one 64 B row), verifies the
+// first live candidate with text[pos + j], text[pos + j + 4] and reads its
+// draft tokens m + j + 4k (k < 8) in the same round trip.  Groups the first
+// row does not decide (the key lies further along the probe sequence, or the
+// first candidate fails its text check) take a row loop.
+__global__ void __launch_bounds__(256, 8) k_draft4(HsIndexView V, int32_t n_seq, const int32_t* __restrict__ slot_of_seq,
+                                                const int32_t* __restrict__ gen_tok, int32_t gen_stride,
+                                                const int32_t* __restrict__ gen_len,
+                                                const int32_t* __restrict__ prefix_len,
+                                                const int32_t* __restrict__ window,
+                                                const uint8_t* __restrict__ speculate,
+                                                int32_t* __restrict__ draft_tok, int32_t draft_stride,
+                                                int32_t* __restrict__ draft_len, uint8_t* __restrict__ looked,
+                                                uint8_t* __restrict__ found) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, j = lane & 3;
+  int64_t s = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 8 + g;
+  const bool valid = s < n_seq;
+  if (!valid) s = n_seq - 1;   // keep the whole warp converged; results discarded
+  const int32_t m = prefix_len[s], pos = gen_len[s], slot = slot_of_seq[s];
+  const int32_t win = window[s];
+  const bool look = valid && speculate[s] && slot >= 0 && pos >= m && V.table && m >= V.prefix_min &&
+                    m <= V.prefix_max;
+  const int32_t* prow = gen_tok + s * (int64_t)gen_stride + pos - m;
+  const int32_t pre_a = (look && j < m) ? prow[j] : 0;
+  const int32_t pre_b = (look && j + 4 < m) ? prow[j + 4] : 0;
+  // polynomial hash: terms j and j + 4 per lane, 2-step butterfly inside the 4 lanes
+  uint64_t term = 0ull;
+  if (look && j < m) term += gram_term(pre_a, j);
+  if (look && j + 4 < m) term += gram_term(pre_b, j + 4);
+  term += __shfl_xor_sync(0xffffffffu, term, 2);
+  term += __shfl_xor_sync(0xffffffffu, term, 1);
+  const uint64_t h = mix64(gram_seed(slot, m) + term);
+  const int32_t tag = gram_tag(h, m);
+  const int64_t lo = look ? V.slot_text_off[slot] : 0, hi = look ? V.slot_text_off[slot + 1] : 0;
+  const int64_t base = (int64_t)(h & (uint64_t)V.table_mask);
+  auto group_or = [&](unsigned v) {
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    return v;
+  };
+  // one table row: probe-ordered 8-bit masks of empty slots and live candidates (before the first empty)
+  auto probe_row = [&](int64_t b, bool active, HsGramEntry& e0, HsGramEntry& e1, unsigned& em, unsigned& cm) {
+    e0.pos = e1.pos = -1;
+    e0.tag = e1.tag = 0;
+    if (active) {
+      e0 = V.table[(b + 2 * j) & V.table_mask];
+      e1 = V.table[(b + 2 * j + 1) & V.table_mask];
+    }
+    const bool c0 = e0.pos >= 0 && e0.tag == tag && e0.pos >= lo && e0.pos < hi;
+    const bool c1 = e1.pos >= 0 && e1.tag == tag && e1.pos >= lo && e1.pos < hi;
+    em = group_or(((e0.pos < 0) ? 1u : 0u) << (2 * j) | ((e1.pos < 0) ? 2u : 0u) << (2 * j));
+    cm = group_or((c0 ? 1u : 0u) << (2 * j) | (c1 ? 2u : 0u) << (2 * j));
+    if (!active) {
+      em = 1u;
+      cm = 0u;
+    }
+    cm &= em ? ((1u << (__ffs(em) - 1)) - 1u) : 0xFFu;
+  };
+  auto cand_pos = [&](unsigned cm, const HsGramEntry& e0, const HsGramEntry& e1) {
+    const int c = cm ? __ffs(cm) - 1 : 0;
+    const int src = (g << 2) + (c >> 1);
+    const int32_t p0 = __shfl_sync(0xffffffffu, e0.pos, src), p1 = __shfl_sync(0xffffffffu, e1.pos, src);
+    return (c & 1) ? p1 : p0;
+  };
+  auto mismatch = [&](bool active, int32_t cp) {
+    bool bad = false;
+    if (active) {
+      const int32_t va = j < m ? V.text[cp + j] : 0, vb = j + 4 < m ? V.text[cp + j + 4] : 0;
+      bad = (j < m && va != pre_a) || (j + 4 < m && vb != pre_b);
+    }
+    return group_or(bad ? 1u : 0u) != 0u;
+  };
+  int32_t hit_pos = -1;
+  int32_t t8[8];   // draft tokens text[hit_pos + m + j + 4k]
+  bool have = false;
+  // first row, fused: the first live candidate's verify and draft tokens in one round trip
+  HsGramEntry e0, e1;
+  unsigned em, cm;
+  probe_row(base, look, e0, e1, em, cm);
+  bool done = !look;
+  {
+    const int32_t cp = cand_pos(cm, e0, e1);
+    bool bad = false;
+    int32_t va = 0, vb = 0;
+    if (cm) {
+      va = j < m ? V.text[cp + j] : 0;
+      vb = j + 4 < m ? V.text[cp + j + 4] : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t8[k] = j + 4 * k < win ? V.text[cp + m + j + 4 * k] : 0;
+      bad = (j < m && va != pre_a) || (j + 4 < m && vb != pre_b);
+    }
+    const bool anybad = group_or(bad ? 1u : 0u) != 0u;
+    if (cm && !anybad) {
+      hit_pos = cp;
+      have = true;
+      done = true;
+    } else if (!cm && em) {
+      done = true;   // an empty slot before any candidate: the key is absent
+    }
+  }
+  // undecided groups: probe rows from the start, candidates in probe order
+  for (int64_t b = base; __any_sync(0xffffffffu, !done); b += 8) {
+    probe_row(b, !done, e0, e1, em, cm);
+    while (__any_sync(0xffffffffu, cm != 0u)) {
+      const int32_t cp = cand_pos(cm, e0, e1);
+      const bool bad = mismatch(cm != 0u, cp);
+      if (cm) {
+        if (!bad) {
+          hit_pos = cp;
+          cm = 0u;
+          em = 1u;   // resolved
+        } else {
+          cm &= cm - 1u;
+        }
+      }
+    }
+    if (!done && (hit_pos >= 0 || em)) done = true;
+  }
+  const bool hit = hit_pos >= 0;
+  if (hit && !have) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t8[k] = j + 4 * k < win ? V.text[hit_pos + m + j + 4 * k] : 0;
+  }
+  int32_t first_term = 32;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int idx = j + 4 * k;
+    if (hit && idx < win && t8[k] < 0 && idx < first_term) first_term = idx;
+  }
+  first_term = min(first_term, __shfl_xor_sync(0xffffffffu, first_term, 1));
+  first_term = min(first_term, __shfl_xor_sync(0xffffffffu, first_term, 2));
+  const int32_t len = hit ? min(first_term, win) : 0;
+  if (valid) {
+    int32_t* out = draft_tok + s * (int64_t)draft_stride;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = j + 4 * k;
+      if (idx < len) out[idx] = t8[k];
+    }
+    if (j == 0) {
+      draft_len[s] = len;
+      looked[s] = valid && speculate[s] && slot >= 0 && pos >= m;
+      found[s] = hit;
+    }
+  }
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -394,10 +547,19 @@ extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d
   // every prefix length the caller can produce is tabled and <= 8, windows <= 32: 8-lane groups
   if (V.table && prefix_lo >= V.prefix_min && prefix_hi <= V.prefix_max && prefix_hi <= 8 && window_hi <= 32 &&
       draft_stride >= window_hi) {
+    hs_count_launches(1);
+    static const bool lanes8 = getenv("HS_K2_DRAFT8") != nullptr;     // A/B switches for profiling only
+    static const bool unfused = getenv("HS_K2_UNFUSED") != nullptr;
+    if (!lanes8) {
+      const int64_t warps4 = ((int64_t)n_seq + 7) / 8;
+      k_draft4<<<(unsigned)((warps4 * 32 + threads - 1) / threads), threads, 0, (cudaStream_t)stream>>>(
+          V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride, d_gen_len, d_prefix_len, d_window, d_speculate,
+          d_draft_tok, draft_stride, d_draft_len, d_looked, d_found);
+      HS_CUDA_TRY(cudaGetLastError());
+      return HS_OK;
+    }
     int64_t warps = ((int64_t)n_seq + 3) / 4;
     int64_t blocks8 = (warps * 32 + threads - 1) / threads;
-    hs_count_launches(1);
-    static const bool unfused = getenv("HS_K2_UNFUSED") != nullptr;   // A/B switch for profiling only
     auto kern = unfused ? k_draft8<false> : k_draft8<true>;
     kern<<<(unsigned)blocks8, threads, 0, (cudaStream_t)stream>>>(V, n_seq, d_slot_of_seq, d_gen_tok, gen_stride,
                                                                   d_gen_len, d_prefix_len, d_window, d_speculate,

@@ -327,7 +327,7 @@ __global__ void k_table_insert(Sparse S, const int32_t* __restrict__ lcp, const 
                                const int64_t* __restrict__ wsum, const int32_t* __restrict__ heavy,
                                const int32_t* __restrict__ rid, const int32_t* __restrict__ resp_slot,
                                int64_t n, int32_t mmin, int32_t mmax, HsGramEntry* __restrict__ table,
-                               int64_t mask) {
+                               int64_t* __restrict__ table_mass, int64_t mask) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int32_t p = sa[k], r = rem[p], v = lcp[k];
@@ -350,7 +350,7 @@ __global__ void k_table_insert(Sparse S, const int32_t* __restrict__ lcp, const 
       int32_t old = atomicCAS(&table[idx].pos, -1, h);
       if (old == -1) {
         table[idx].tag = tag;
-        table[idx].mass = mass;
+        table_mass[idx] = mass;
         break;
       }
       idx = (idx + 1) & mask;
@@ -721,7 +721,7 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
 extern "C" int hs_index_table_bytes(const HsIndexView* view, size_t* bytes) {
   int64_t cap = 1024;
   while (cap < 2 * view->n_gram_groups) cap <<= 1;
-  *bytes = sizeof(HsGramEntry) * (size_t)cap;
+  *bytes = (sizeof(HsGramEntry) + sizeof(int64_t)) * (size_t)cap;   // entries, then the parallel masses
   return HS_OK;
 }
 
@@ -730,9 +730,10 @@ extern "C" int hs_index_build_table(HsIndexView* view, void* d_table, size_t tab
   size_t need;
   hs_index_table_bytes(view, &need);
   if (table_bytes < need) { hs_set_error("table buffer too small"); return HS_ERR_SPACE; }
-  int64_t cap = (int64_t)(need / sizeof(HsGramEntry));
+  int64_t cap = (int64_t)(need / (sizeof(HsGramEntry) + sizeof(int64_t)));
   HsGramEntry* table = (HsGramEntry*)d_table;
-  HS_CUDA_TRY(cudaMemsetAsync(table, 0xFF, need, st));
+  int64_t* table_mass = reinterpret_cast<int64_t*>(table + cap);
+  HS_CUDA_TRY(cudaMemsetAsync(table, 0xFF, sizeof(HsGramEntry) * (size_t)cap, st));   // pos = -1: empty
   int64_t n = view->n_suffix;
   if (n > 0) {
     // rebuild the workspace layout to find rid / rem / sparse levels
@@ -750,7 +751,7 @@ extern "C" int hs_index_build_table(HsIndexView* view, void* d_table, size_t tab
     hs_count_launches(1);
     k_table_insert<<<blocks(n), 256, 0, st>>>(S, view->lcp, view->sa, L.rem, view->text, view->wsum, view->heavy,
                                               L.rid, L.resp_slot, n, view->prefix_min, view->prefix_max, table,
-                                              cap - 1);
+                                              table_mass, cap - 1);
     HS_CUDA_TRY(cudaGetLastError());
   }
   view->table = table;

@@ -8,7 +8,7 @@ responses).  HBM layout (all slot-major):
   lcp    int32 [sum(len) + 1]             -1 at slot boundaries
   wsum   int64 [sum(len) + 1]             prefix sums of reward fixed point (2^-32)
   heavy  int32 [sum(len)]                 heavy (greedy) continuation per LCP node
-  table  16 B x 2^k                       (slot, m, m-gram) -> (heavy pos, mass)
+  table  (8 + 8) B x 2^k                 (slot, m, m-gram) -> heavy pos [+ tag]; mass in a parallel array
 
 Replaces `rhymesim/history.py:343-355 build_tree` (+ `SuffixTree.add_response`
 / `finalize`, :148-279) for many prompts in one launch sequence.
