@@ -149,6 +149,20 @@ class Dist:
             self.pg.destroy_process_group()
 
 
+def measured_traffic(key, applies=True):
+    """Per-launch DRAM traffic (read + write bytes) of `key` from the committed ncu capture
+    (profiles/r01_traffic.json), or None when absent or when this run's workload is not the captured one."""
+    if not applies:
+        return None, None
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f).get(key)
+    except (OSError, ValueError):
+        return None, None
+    return (ent["bytes"], "ncu --set full, profiles/r01_traffic.json: " + ent["launch"]) if ent else (None, None)
+
+
 def timed(fn, steps, warmup, dist, stream, gpu_index):
     """W untimed + exactly K timed calls bracketed by barrier + synchronize; returns (ms/step, clocks)."""
     import torch
@@ -472,6 +486,8 @@ def run_rollout(args, dist, pk):
         ach = kvb / (k_ms / 1e3) / 1e9
         roof = {"kernel": label, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "traffic": None}
+    std_cfg = (B, P, T, args.samples) == (1024, 256, 4096, 8) and dist.world == 1
+    roof["traffic"], roof["traffic_source"] = measured_traffic("rollout:" + label, std_cfg)
     roof["peak_source"] = pk["source"] + (" sustained" if roof["unit"] == "TFLOP/s" else "")
     distinct = len({tuple(base.tokens[b, i:i + 4]) for b in range(0, B, S) for i in range(0, T - 4, 7)})
     distinct /= max(1, len(range(0, B, S)) * len(range(0, T - 4, 7)))
@@ -568,7 +584,9 @@ def run_lookup(args, dist, pk):
                    "l2": "index + outputs exceed L2"},
         "hit_rate": hits / n, "mean_draft_len": dl / n,
         "roofline": {"kernel": "k_draft", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "traffic": measured_traffic("lookup:k_draft", (P, L) == (512, 4096))[0],
+                     "traffic_source": measured_traffic("lookup:k_draft", (P, L) == (512, 4096))[1],
                      "bytes_per_query": alg / n},
         "gpu_launches": 1, "clocks": clocks,
     }, data
