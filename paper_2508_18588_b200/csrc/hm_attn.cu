@@ -262,8 +262,12 @@ __global__ void __launch_bounds__(128) k_attention(const __nv_bfloat16* __restri
 // SL=2; decode: SL=1) and keeps every warp busy.  The key->warp map depends
 // only on the key position and the merge order is fixed, so a row's result is
 // independent of the batch (bit-exact greedy under speculation).
-template <int HD, int SL>
-__global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restrict__ q,
+// NW = 8 (with SL = 2): eight warps, warp w = (key group w & 3, slice w >> 2) -- one 16-row slice per
+// warp instead of two, half the registers, so two CTAs (16 warps) fit an SM.  The per-slice source is
+// the same as NW = 4's and the rounding is pinned with explicit intrinsics, so a row's bits do not
+// depend on NW (or on SL): verify blocks and decode rows still agree bit for bit.
+template <int HD, int SL, int NW = 4>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_attention2(const __nv_bfloat16* __restrict__ q,
                                                     const __nv_bfloat16* __restrict__ kc,
                                                     const __nv_bfloat16* __restrict__ vc, int64_t slot_stride,
                                                     const int32_t* __restrict__ q_off,
@@ -279,8 +283,12 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   constexpr int ROWS = 16 * SL;
   constexpr int KS = 64;            // keys per stage (4 warps x 16)
   constexpr int NST = 3;            // pipeline stages
+  static_assert(NW == 4 || (NW == 8 && SL == 2), "8 warps: one slice each of a 2-slice tile");
+  constexpr int SLW = NW == 8 ? 1 : SL;   // slices this warp computes
   const int G = H / KVH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kg = warp & 3;                                // key group: keys [stage * 64 + 16 kg, +16)
+  const int sl_base = NW == 8 ? (warp >> 2) : 0;          // first slice of this warp
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   // TMA 128B-swizzled destinations need 1024-byte alignment (the launch adds 1 KB of slack)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -359,27 +367,27 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
       cp_commit();
     }
   }
-  int rpos[SL][2];
-  // per slice: live (any row < rows_total; a slice of padding rows only is skipped -- its state is
-  // never merged into an output row) and vis_all (keys <= vis_all are visible to all 16 rows, so
-  // their blocks skip the mask: the mask is the identity there).  Both warp-uniform, both exact.
-  bool live[SL];
-  int vis_all[SL];
+  int rpos[SLW][2];
+  // per slice of this warp: live (any row < rows_total; a slice of padding rows only is skipped -- its
+  // state is never merged into an output row) and vis_all (keys <= vis_all are visible to all 16 rows,
+  // so their blocks skip the mask: the mask is the identity there).  Both warp-uniform, both exact.
+  bool live[SLW];
+  int vis_all[SLW];
 #pragma unroll
-  for (int sl = 0; sl < SL; ++sl) {
+  for (int sl = 0; sl < SLW; ++sl) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int rr = tile * ROWS + sl * 16 + (lane >> 2) + 8 * h;
+      const int rr = tile * ROWS + (sl_base + sl) * 16 + (lane >> 2) + 8 * h;
       rpos[sl][h] = rr < rows_total ? p0 + rr / G : -1;   // -1: padding row, fully masked
     }
-    const int first = tile * ROWS + sl * 16;
+    const int first = tile * ROWS + (sl_base + sl) * 16;
     live[sl] = first < rows_total;
     vis_all[sl] = first + 15 < rows_total ? p0 + first / G : -1;
   }
-  float o[SL][HD / 8][4];
-  float mrow[SL][2], lrow[SL][2];
+  float o[SLW][HD / 8][4];
+  float mrow[SLW][2], lrow[SLW][2];
 #pragma unroll
-  for (int sl = 0; sl < SL; ++sl) {
+  for (int sl = 0; sl < SLW; ++sl) {
 #pragma unroll
     for (int i = 0; i < HD / 8; ++i) o[sl][i][0] = o[sl][i][1] = o[sl][i][2] = o[sl][i][3] = 0.f;
     mrow[sl][0] = mrow[sl][1] = -INFINITY;
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   // slices of padding rows only are skipped: their state never reaches an output row).  The live
   // slices share every K and V fragment load, and their independent mma/softmax chains interleave.
   // Per slice the arithmetic is identical for every NS and SL (a row's bits do not depend on the tile).
-  auto stages = [&](auto ns_tag) {
+  auto stages = [&](auto ns_tag, bool compute) {
     constexpr int NS = decltype(ns_tag)::value;
     for (int st = 0; st < n_stage; ++st) {
       int buf;
@@ -406,8 +414,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         cp_commit();
         buf = st % NST;
       }
-      const int key0 = st * KS + warp * 16;
-      if (key0 > max_pos) continue;   // warp-uniform
+      const int key0 = st * KS + kg * 16;
+      if (!compute || key0 > max_pos) continue;   // warp-uniform
       const uint4* K = sK + (buf * KS) * CH;
       const uint4* V = sV + (buf * KS) * CH;
       float sc[NS][2][4];
@@ -420,14 +428,14 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         uint32_t kb[2][4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
-          ldsm_x4(kb[j][0], kb[j][1], kb[j][2], kb[j][3], &K[kvoff(warp * 16 + j * 8 + (lane & 7), c * 4 + (lane >> 3))]);
+          ldsm_x4(kb[j][0], kb[j][1], kb[j][2], kb[j][3], &K[kvoff(kg * 16 + j * 8 + (lane & 7), c * 4 + (lane >> 3))]);
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
           uint32_t qa[2][4];
 #pragma unroll
           for (int u = 0; u < 2; ++u)
             ldsm_x4(qa[u][0], qa[u][1], qa[u][2], qa[u][3],
-                    &sQ[swz<HD>(sl * 16 + (lane & 15), (2 * c + u) * 2 + (lane >> 4))]);
+                    &sQ[swz<HD>((sl_base + sl) * 16 + (lane & 15), (2 * c + u) * 2 + (lane >> 4))]);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             mma16816(sc[sl][j], qa[0], kb[j][0], kb[j][1]);
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
           for (int j = 0; j < 2; ++j) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              sc[sl][j][e] *= scale_log2;
-              sc[sl][j][2 + e] *= scale_log2;
+              sc[sl][j][e] = __fmul_rn(sc[sl][j][e], scale_log2);
+              sc[sl][j][2 + e] = __fmul_rn(sc[sl][j][2 + e], scale_log2);
               bm0 = fmaxf(bm0, sc[sl][j][e]);
               bm1 = fmaxf(bm1, sc[sl][j][2 + e]);
             }
@@ -456,8 +464,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int key = key0 + j * 8 + 2 * (lane & 3) + e;
-              sc[sl][j][e] = key <= rpos[sl][0] ? sc[sl][j][e] * scale_log2 : -INFINITY;
-              sc[sl][j][2 + e] = key <= rpos[sl][1] ? sc[sl][j][2 + e] * scale_log2 : -INFINITY;
+              sc[sl][j][e] = key <= rpos[sl][0] ? __fmul_rn(sc[sl][j][e], scale_log2) : -INFINITY;
+              sc[sl][j][2 + e] = key <= rpos[sl][1] ? __fmul_rn(sc[sl][j][2 + e], scale_log2) : -INFINITY;
               bm0 = fmaxf(bm0, sc[sl][j][e]);
               bm1 = fmaxf(bm1, sc[sl][j][2 + e]);
             }
@@ -468,26 +476,26 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
         bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
         const float nm0 = fmaxf(mrow[sl][0], bm0), nm1 = fmaxf(mrow[sl][1], bm1);
-        const float a0 = nm0 == -INFINITY ? 1.f : exp2f(mrow[sl][0] - nm0);
-        const float a1 = nm1 == -INFINITY ? 1.f : exp2f(mrow[sl][1] - nm1);
+        const float a0 = nm0 == -INFINITY ? 1.f : exp2f(__fsub_rn(mrow[sl][0], nm0));
+        const float a1 = nm1 == -INFINITY ? 1.f : exp2f(__fsub_rn(mrow[sl][1], nm1));
         const float sub0 = nm0 == -INFINITY ? 0.f : nm0;
         const float sub1 = nm1 == -INFINITY ? 0.f : nm1;
         float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          sc[sl][j][0] = exp2f(sc[sl][j][0] - sub0);
-          sc[sl][j][1] = exp2f(sc[sl][j][1] - sub0);
-          sc[sl][j][2] = exp2f(sc[sl][j][2] - sub1);
-          sc[sl][j][3] = exp2f(sc[sl][j][3] - sub1);
-          rs0 += sc[sl][j][0] + sc[sl][j][1];
-          rs1 += sc[sl][j][2] + sc[sl][j][3];
+          sc[sl][j][0] = exp2f(__fsub_rn(sc[sl][j][0], sub0));
+          sc[sl][j][1] = exp2f(__fsub_rn(sc[sl][j][1], sub0));
+          sc[sl][j][2] = exp2f(__fsub_rn(sc[sl][j][2], sub1));
+          sc[sl][j][3] = exp2f(__fsub_rn(sc[sl][j][3], sub1));
+          rs0 = __fadd_rn(rs0, __fadd_rn(sc[sl][j][0], sc[sl][j][1]));
+          rs1 = __fadd_rn(rs1, __fadd_rn(sc[sl][j][2], sc[sl][j][3]));
         }
-        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
-        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
-        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
-        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
-        lrow[sl][0] = lrow[sl][0] * a0 + rs0;
-        lrow[sl][1] = lrow[sl][1] * a1 + rs1;
+        rs0 = __fadd_rn(rs0, __shfl_xor_sync(0xffffffffu, rs0, 1));
+        rs0 = __fadd_rn(rs0, __shfl_xor_sync(0xffffffffu, rs0, 2));
+        rs1 = __fadd_rn(rs1, __shfl_xor_sync(0xffffffffu, rs1, 1));
+        rs1 = __fadd_rn(rs1, __shfl_xor_sync(0xffffffffu, rs1, 2));
+        lrow[sl][0] = __fmaf_rn(lrow[sl][0], a0, rs0);
+        lrow[sl][1] = __fmaf_rn(lrow[sl][1], a1, rs1);
         mrow[sl][0] = nm0;
         mrow[sl][1] = nm1;
         pa[sl][0] = pack2(sc[sl][0][0], sc[sl][0][1]);
@@ -498,17 +506,17 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         if (!(flags & 1) || __any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
 #pragma unroll
           for (int n = 0; n < HD / 8; ++n) {
-            o[sl][n][0] *= a0;
-            o[sl][n][1] *= a0;
-            o[sl][n][2] *= a1;
-            o[sl][n][3] *= a1;
+            o[sl][n][0] = __fmul_rn(o[sl][n][0], a0);
+            o[sl][n][1] = __fmul_rn(o[sl][n][1], a0);
+            o[sl][n][2] = __fmul_rn(o[sl][n][2], a1);
+            o[sl][n][3] = __fmul_rn(o[sl][n][3], a1);
           }
         }
       }
 #pragma unroll
       for (int n = 0; n < HD / 16; ++n) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(warp * 16 + (lane & 15), n * 2 + (lane >> 4))]);
+        ldsm_x4_t(b0, b1, b2, b3, &V[kvoff(kg * 16 + (lane & 15), n * 2 + (lane >> 4))]);
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
           mma16816(o[sl][2 * n], pa[sl], b0, b1);
@@ -517,11 +525,12 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
       }
     }
   };
-  if constexpr (SL == 1) {
-    stages(std::integral_constant<int, 1>{});
+  if constexpr (SLW == 1) {
+    // NW = 8: a warp whose slice is padding only still walks the stages (barriers, TMA issue)
+    stages(std::integral_constant<int, 1>{}, live[0] || !(flags & 2));
   } else {
-    if ((flags & 2) && !live[1]) stages(std::integral_constant<int, 1>{});
-    else stages(std::integral_constant<int, SL>{});
+    if ((flags & 2) && !live[1]) stages(std::integral_constant<int, 1>{}, true);
+    else stages(std::integral_constant<int, SLW>{}, true);
   }
   cp_wait<0>();
   __syncthreads();
@@ -532,11 +541,11 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
   float* cM = cO + 4 * ROWS * HD;                            // [4][ROWS]
   float* cL = cM + 4 * ROWS;                                 // [4][ROWS]
 #pragma unroll
-  for (int sl = 0; sl < SL; ++sl) {
+  for (int sl = 0; sl < SLW; ++sl) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = sl * 16 + (lane >> 2) + 8 * h;
-      float* dst = cO + ((size_t)warp * ROWS + r) * HD;
+      const int r = (sl_base + sl) * 16 + (lane >> 2) + 8 * h;
+      float* dst = cO + ((size_t)kg * ROWS + r) * HD;
 #pragma unroll
       for (int i = 0; i < HD / 8; ++i) {
         const int col = i * 8 + 2 * (lane & 3);
@@ -544,8 +553,8 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
         dst[col + 1] = o[sl][i][2 * h + 1];
       }
       if ((lane & 3) == 0) {
-        cM[warp * ROWS + r] = mrow[sl][h];
-        cL[warp * ROWS + r] = lrow[sl][h];
+        cM[kg * ROWS + r] = mrow[sl][h];
+        cL[kg * ROWS + r] = lrow[sl][h];
       }
     }
   }
@@ -561,10 +570,10 @@ __global__ void __launch_bounds__(128) k_attention2(const __nv_bfloat16* __restr
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
       const float mw = cM[w * ROWS + r];
-      const float sc = mw == -INFINITY ? 0.f : exp2f(mw - mx);
-      den += cL[w * ROWS + r] * sc;
-      num0 += cO[((size_t)w * ROWS + r) * HD + d] * sc;
-      num1 += cO[((size_t)w * ROWS + r) * HD + d + 1] * sc;
+      const float sc = mw == -INFINITY ? 0.f : exp2f(__fsub_rn(mw, mx));
+      den = __fmaf_rn(cL[w * ROWS + r], sc, den);
+      num0 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d], sc, num0);
+      num1 = __fmaf_rn(cO[((size_t)w * ROWS + r) * HD + d + 1], sc, num1);
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
     __nv_bfloat16* dst = out + ((size_t)(qo + rr / G) * H + kvh * G + rr % G) * HD + d;
@@ -687,6 +696,25 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
     if (!work_ready) {
       k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
       hm_count_launches(1);
+    }
+    if constexpr (SL == 2) {
+      // verify tiles, opt-in (HM_ATTN_W8): the 8-warp variant (one slice per warp, two CTAs per SM), same
+      // bits as NW = 4.  Measured on the real verify mix it is no faster: 46% more instructions (each
+      // warp loads its own K/V fragments) cancel the doubled warps (profiles/r01_attention_variants.md)
+      static const bool w8 = getenv("HM_ATTN_W8") != nullptr;
+      if (w8) {
+        static int occ8 = 0;
+        if (!occ8) {
+          cudaFuncSetAttribute(k_attention2<HD, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, k_attention2<HD, 2, 8>, 256, smem);
+          if (occ8 < 1) occ8 = 1;
+        }
+        k_attention2<HD, 2, 8><<<n_sm * occ8, 256, smem, st>>>(
+            (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
+            d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
+            mk, mv, use_tma, attn_flags());
+        return 0;
+      }
     }
     k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,

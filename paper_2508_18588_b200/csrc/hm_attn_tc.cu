@@ -274,7 +274,9 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
         const int it_next = it + gridDim.x;
         MBAR_WAIT(&q_full[items & 1], (items >> 1) & 1, 3, (int)g);   // this item's Q tile is in smem
         tc_fence_after();
-        for (int i = 0; i < NS && i < n_stage; ++i) issue_s(g + i);
+        // S runs NS - 1 stages ahead of P.V: the buffer S_{j+2} overwrites held P_{j-1}, whose P.V was
+        // queued a stage earlier, so the issuing thread rarely waits (S_{j+3} would wait for P_j.V_j)
+        for (int i = 0; i < NS - 1 && i < n_stage; ++i) issue_s(g + i);
         const int n_next = it_next < n_items ? stages_of(it_next) : 0;   // its loads overlap the S MMAs
         if (items > 0) {   // the previous item's epilogue has read O
           MBAR_WAIT(&o_free, (items - 1) & 1, 4, (int)g);
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
           umma_commit(&v_empty[vslot]);
           umma_commit(&p_done[b]);
           if (st == n_stage - 1) umma_commit(&o_ready);   // the item's O is complete
-          if (st + NS < n_stage) issue_s(gs + NS);
+          if (st + NS - 1 < n_stage) issue_s(gs + NS - 1);
         }
         g += n_stage;
         it = it_next;
