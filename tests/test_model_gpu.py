@@ -377,7 +377,7 @@ def test_qwen_shape_engine_spec_equals_greedy(torch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("family", ["mma_sync", "tcgen05"])
+@pytest.mark.parametrize("family", ["mma_sync", "mma_sync_w8", "tcgen05"])
 def test_attention_family_subprocess(family):
     """Each attention kernel family (chosen per process) against the fp32 reference, decode-row
     invariance and spec == greedy, in a fresh interpreter."""
@@ -387,8 +387,11 @@ def test_attention_family_subprocess(family):
     env = dict(os.environ)
     env.pop("HM_ATTN_TC", None)
     env.pop("HM_ATTN_V2", None)
+    env.pop("HM_ATTN_W8", None)
     if family == "tcgen05":
         env["HM_ATTN_TC"] = "1"
+    if family == "mma_sync_w8":
+        env["HM_ATTN_W8"] = "1"
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, os.path.join(here, "attn_family_check.py")], env=env, capture_output=True,
                        text=True, timeout=600)
