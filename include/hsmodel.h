@@ -92,6 +92,13 @@ int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, in
                  int32_t work_ready /* d_work already holds hm_attention_plan's output */,
                  int32_t n_slots /* cache slots, > 0 enables TMA loads */, hm_stream_t stream);
 
+/* Attention kernel family for the forwards that follow (process-wide): 0 = mma.sync m16n8k16
+ * (4 warps split each 64-key stage), 1 = tcgen05 (TMEM S/P/O, 128-row tiles, 128-key stages; the
+ * default).  Both are batch invariant; rows from different families differ in their last bits, so
+ * a speculative rollout and the greedy run it is compared with use one family. */
+int hm_set_attention_family(int32_t family);
+int hm_attention_family(void);
+
 /* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent). */
 int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                       int32_t* d_work, hm_stream_t stream);

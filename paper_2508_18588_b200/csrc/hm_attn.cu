@@ -637,19 +637,26 @@ __global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G
   if (threadIdx.x == 0) work[n_seq] = carry;
 }
 
-// tcgen05 attention (hm_attn_tc.cu), opt-in with HM_ATTN_TC=1 while its decode throughput is below the
-// mma.sync kernels' (it needs a work list and the cache geometry for the TMA maps); both families are
-// batch invariant, but a run must not mix them (speculative and greedy rows must share one kernel family)
+// tcgen05 attention (hm_attn_tc.cu): the default family (hm_set_attention_family; HM_ATTN_MMA selects
+// mma.sync).  It needs a work list and the cache geometry for the TMA maps, else the mma.sync kernels
+// run.  Both families are batch invariant, but a run must not mix them (speculative and greedy rows
+// must share one kernel family)
 constexpr int kTcRows = 128;
 constexpr int kTcKeys = 128;   // keys per K/V stage: the TMA box height of the tcgen05 path
 template <int HD>
 int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                    const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
                    void* d_out, const int32_t* d_work, const CUtensorMap& mk, const CUtensorMap& mv,
-                   cudaStream_t st);
+                   const CUtensorMap& mk64, const CUtensorMap& mv64, cudaStream_t st);
+// attention family: -1 = not chosen yet (environment default), 0 = mma.sync, 1 = tcgen05 (hm_set_attention_family)
+inline int& attn_family() {
+  static int family = -1;
+  return family;
+}
 inline bool attn_tc_enabled() {
-  static const bool on = getenv("HM_ATTN_TC") != nullptr && getenv("HM_ATTN_V2") == nullptr;
-  return on;
+  if (attn_family() < 0)   // default tcgen05; HM_ATTN_MMA / HM_ATTN_V2 select mma.sync (A/B)
+    attn_family() = (getenv("HM_ATTN_MMA") != nullptr || getenv("HM_ATTN_V2") != nullptr) ? 0 : 1;
+  return attn_family() == 1;
 }
 
 // exact work skips of k_attention2 (bit 0: rescale only when a row max moved, bit 1: skip slices
@@ -732,6 +739,16 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
 
 }  // namespace hm
 
+// Attention kernel family for the forwards that follow (process-wide): 0 = mma.sync, 1 = tcgen05.  Both
+// are batch invariant, but rows computed by different families differ in their last bits, so one
+// rollout (and the greedy run it is compared with) must use one family.
+extern "C" int hm_set_attention_family(int32_t family) {
+  if (family != 0 && family != 1) { hm_set_error("attention family must be 0 (mma.sync) or 1 (tcgen05)"); return HM_ERR_INVALID; }
+  hm::attn_family() = family;
+  return HM_OK;
+}
+extern "C" int hm_attention_family(void) { return hm::attn_tc_enabled() ? 1 : 0; }
+
 // Work list of the persistent attention kernel, computed once per forward (q_len is the same for
 // every layer): work[s] = first tile of sequence s, work[n_seq] = total tiles.
 extern "C" int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
@@ -761,21 +778,23 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
   cudaStream_t st = (cudaStream_t)stream;
   if (hm::attn_tc_enabled()) {
     // tcgen05 path: needs the persistent work list and the cache geometry for the TMA maps
-    CUtensorMap mk, mv;
+    CUtensorMap mk, mv, mk64, mv64;   // full 128-key stage boxes and the trimmed last-stage boxes
     const int64_t rows = (int64_t)n_slots * KVH * max_len;
     if (d_work && n_slots > 0 && (hd == 128 || hd == 64) &&
         hm_make_tma_map(&mk, d_kcache, rows, hd, hd, hm::kTcKeys) &&
-        hm_make_tma_map(&mv, d_vcache, rows, hd, hd, hm::kTcKeys)) {
+        hm_make_tma_map(&mv, d_vcache, rows, hd, hd, hm::kTcKeys) &&
+        hm_make_tma_map(&mk64, d_kcache, rows, hd, hd, hm::kTcKeys / 2) &&
+        hm_make_tma_map(&mv64, d_vcache, rows, hd, hd, hm::kTcKeys / 2)) {
       if (!work_ready) {
         hm::k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, hm::kTcRows, d_work);
         hm_count_launches(1);
       }
       if (hd == 128)
         hm::launch_attn_tc<128>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
-                                d_work, mk, mv, st);
+                                d_work, mk, mv, mk64, mv64, st);
       else
         hm::launch_attn_tc<64>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
-                               d_work, mk, mv, st);
+                               d_work, mk, mv, mk64, mv64, st);
       hm_count_launches(1);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }

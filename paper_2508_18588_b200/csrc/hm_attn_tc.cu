@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
                                                     int max_len, float scale_log2, __nv_bfloat16* __restrict__ out,
                                                     int n_seq, const int32_t* __restrict__ work,
                                                     const __grid_constant__ CUtensorMap tmK,
-                                                    const __grid_constant__ CUtensorMap tmV) {
+                                                    const __grid_constant__ CUtensorMap tmV,
+                                                    const __grid_constant__ CUtensorMap tmK64,
+                                                    const __grid_constant__ CUtensorMap tmV64) {
   using C = TcAttn<HD>;
   constexpr int ROWS = C::ROWS, KS = C::KS, NSK = C::NSK, NSV = C::NSV, NS = C::NS;
   const int G = H / KVH;
@@ -160,6 +162,11 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&tmem_base);
+  // A trimmed last stage loads only its first 64 keys; the rest of the slot keeps earlier contents, which
+  // are masked (K) or multiplied by P = 0 (V) -- zero the rings once so they are finite from the start.
+  for (int i = threadIdx.x; i < (NSK + NSV) * C::KVB / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sK)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -187,9 +194,10 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     if (lane == 0) {
       struct Cur {
         int it, st, nst, row0;
+        bool half_last;   // the item's last stage needs at most its first 64 keys
         uint32_t g;
       };
-      Cur ck{(int)blockIdx.x - (int)gridDim.x, 0, 0, 0, 0u}, cv = ck;
+      Cur ck{(int)blockIdx.x - (int)gridDim.x, 0, 0, 0, false, 0u}, cv = ck;
       auto advance = [&](Cur& c) {   // move to a stage to load; false when the CTA's items are exhausted
         while (c.st >= c.nst) {
           c.it += gridDim.x;
@@ -197,10 +205,22 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
           int s, kvh, tile;
           locate(c.it, s, kvh, tile);
           c.nst = item_stages(s, tile);
+          const int last_row = min(q_len[s] * G, (tile + 1) * ROWS) - 1;
+          c.half_last = (pos0[s] + last_row / G) % KS < KS / 2;
           c.row0 = (kv_slot[s] * KVH + kvh) * max_len;
           c.st = 0;
         }
         return true;
+      };
+      // one K or V stage; the item's last stage is trimmed to a 64-key box when that covers it (decode rows
+      // would otherwise over-read ~64 keys per item, ~3% of the KV stream)
+      auto load = [&](const Cur& c, const CUtensorMap* full_map, const CUtensorMap* half_map, uint64_t* bar,
+                      uint8_t* dst) {
+        const bool half = c.half_last && c.st == c.nst - 1;
+        mbar_arrive_expect_tx(bar, half ? C::KVB / 2 : C::KVB);
+#pragma unroll
+        for (int hb = 0; hb < HD / 64; ++hb)
+          tma_load_2d(half ? half_map : full_map, bar, dst + hb * KS * 128, hb * 64, c.row0 + c.st * KS);
       };
       bool kmore = advance(ck), vmore = advance(cv);
       while (kmore || vmore) {
@@ -208,10 +228,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
         if (kmore) {
           const int slot = ck.g % NSK;
           if (ck.g < (uint32_t)NSK || mbar_test(&k_empty[slot], ((ck.g / NSK) - 1) & 1)) {
-            mbar_arrive_expect_tx(&k_full[slot], C::KVB);
-#pragma unroll
-            for (int hb = 0; hb < HD / 64; ++hb)
-              tma_load_2d(&tmK, &k_full[slot], sK + slot * C::KVB + hb * KS * 128, hb * 64, ck.row0 + ck.st * KS);
+            load(ck, &tmK, &tmK64, &k_full[slot], sK + slot * C::KVB);
             ++ck.st;
             ++ck.g;
             kmore = advance(ck);
@@ -220,10 +237,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
         if (vmore) {
           const int slot = cv.g % NSV;
           if (cv.g < (uint32_t)NSV || mbar_test(&v_empty[slot], ((cv.g / NSV) - 1) & 1)) {
-            mbar_arrive_expect_tx(&v_full[slot], C::KVB);
-#pragma unroll
-            for (int hb = 0; hb < HD / 64; ++hb)
-              tma_load_2d(&tmV, &v_full[slot], sV + slot * C::KVB + hb * KS * 128, hb * 64, cv.row0 + cv.st * KS);
+            load(cv, &tmV, &tmV64, &v_full[slot], sV + slot * C::KVB);
             ++cv.st;
             ++cv.g;
             vmore = advance(cv);
@@ -307,17 +321,23 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     }
   } else {
     // ---------------- softmax / correction / epilogue
-    // TMEM lane (= UMMA row = Q row) tl; tile row (tl + 64) mod 128, so the first 64 tile rows -- all of a
-    // decode or short verify block -- sit on quarters 2 and 3, whose SM sub-partitions do not also host the
-    // producer and MMA warps.  Softmax fragment: half h of the quarter, thread t: lanes a = 16h + t/4 and
-    // b = a + 8 (of the quarter), keys 8i + 2q + {0,1}, q = t % 4.
+    // TMEM lane (= UMMA row = Q row) tl of tile row r: 16-row block rb = r / 16 goes to lane quarter
+    // (2 + rb) % 4, half rb / 4.  The first halves of all four quarters fill first, so a tile of up to 64
+    // rows (a verify block of <= 10 queries at GQA-6) spreads over four softmax warps per set, one 16-lane
+    // half each; decode rows sit on quarter 2, whose SM sub-partition does not also host the producer and
+    // MMA warps.  Softmax fragment: half h of the quarter, thread t: lanes a = 16h + t/4 and b = a + 8 (of
+    // the quarter), keys 8i + 2q + {0,1}, q = t % 4.
     const int quarter = warp & 3;
     const int set = (warp - 2) >> 2;   // this set takes the stages with (global stage & 1) == set
     const int tl = quarter * 32 + lane;
-    const int row = (tl + 64) & (ROWS - 1);
+    auto row_of_lane = [&](int ln) {   // inverse of the lane map above
+      const int rb = (((ln >> 5) + 2) & 3) + ((ln >> 4) & 1) * 4;
+      return rb * 16 + (ln & 15);
+    };
+    const int row = row_of_lane(tl);
     const uint32_t t_lane = tbase + ((uint32_t)(quarter * 32) << 16);
     const int q4 = lane & 3;
-    auto trow_of = [&](int h, int ab) { return (quarter * 32 + 16 * h + (lane >> 2) + 8 * ab + 64) & (ROWS - 1); };
+    auto trow_of = [&](int h, int ab) { return row_of_lane(quarter * 32 + 16 * h + (lane >> 2) + 8 * ab); };
     auto lane_of = [&](int h, int ab) { return quarter * 32 + 16 * h + (lane >> 2) + 8 * ab; };
     struct Item {
       int s, kvh, tile, rows_total, rows_here, qo, p0, n_stage;
@@ -369,7 +389,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
       bool hlive[2];    // the half holds a live row (warp-uniform)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        hlive[h] = ((quarter * 32 + 16 * h + 64) & (ROWS - 1)) < rows_here;
+        hlive[h] = row_of_lane(quarter * 32 + 16 * h) < rows_here;   // first row of the half's 16-row block
 #pragma unroll
         for (int ab = 0; ab < 2; ++ab) {
           const int tr = trow_of(h, ab);
@@ -514,7 +534,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
             if (q4 == 0) lbuf[lane_of(h, ab)] += lsum[h][ab];
         __syncwarp();
         const bool live = row < rows_here;
-        if (((tl - lane + 64) & (ROWS - 1)) < rows_here) {   // the warp holds a live row
+        if (hlive[0] || hlive[1]) {   // the warp holds a live row
           const float lrow = lbuf[tl];
           const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
           const int rr = cur.tile * ROWS + row;
@@ -558,7 +578,7 @@ template <int HD>
 int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                    const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
                    void* d_out, const int32_t* d_work, const CUtensorMap& mk, const CUtensorMap& mv,
-                   cudaStream_t st) {
+                   const CUtensorMap& mk64, const CUtensorMap& mv64, cudaStream_t st) {
   static int grid = 0;
   if (!grid) {
     cudaFuncSetAttribute(k_attn_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcAttn<HD>::SMEM);
@@ -569,7 +589,7 @@ int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_l
   }
   k_attn_tc<HD><<<grid, 320, TcAttn<HD>::SMEM, st>>>((const __nv_bfloat16*)d_q, d_q_off, d_q_len, d_pos0, d_kv_slot,
                                                       H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq,
-                                                      d_work, mk, mv);
+                                                      d_work, mk, mv, mk64, mv64);
   return 0;
 }
 
@@ -581,9 +601,9 @@ extern "C" int hm_debug_attn_trace(long long* host_out) {
 
 template int launch_attn_tc<64>(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t,
                                 int32_t, int32_t, int32_t, float, void*, const int32_t*, const CUtensorMap&,
-                                const CUtensorMap&, cudaStream_t);
+                                const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, cudaStream_t);
 template int launch_attn_tc<128>(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int32_t,
                                  int32_t, int32_t, int32_t, float, void*, const int32_t*, const CUtensorMap&,
-                                 const CUtensorMap&, cudaStream_t);
+                                 const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, cudaStream_t);
 
 }  // namespace hm

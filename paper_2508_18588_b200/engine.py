@@ -52,8 +52,10 @@ class RolloutResult:
 class RolloutEngine:
     def __init__(self, cfg: ModelConfig, weights: Weights, n_slots: int, max_len: int, device,
                  spec: SpecConfig | None = None, prefill_rows: int = 16384, use_graphs: bool = True,
-                 check_every: int = 8, temperature: float = 0.0, seed: int = 0):
+                 check_every: int = 8, temperature: float = 0.0, seed: int = 0, attention: str | None = None):
         import torch
+        # attention kernel family ("tcgen05" or "mma_sync"; None: the library default), set per rollout
+        self.attention = attention
         self.use_graphs, self.check_every = use_graphs, check_every
         self.graph_launches = 0   # kernels executed by graph replays (not seen by the C launch counters)
         self.cfg, self.w, self.device = cfg, weights, torch.device(device)
@@ -117,6 +119,9 @@ class RolloutEngine:
         """
         import torch
         from .spec_engine import gate_check
+        if self.attention is not None:
+            from .model import set_attention_family
+            set_attention_family(self.attention)
         prompts = torch.as_tensor(prompts, dtype=torch.int32).to(self.device)
         B, P = prompts.shape
         if recent_acceptance is not None and not gate_check(self.spec.gate(), B, recent_acceptance):

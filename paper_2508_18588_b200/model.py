@@ -40,12 +40,26 @@ SIGNATURES = {
     "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _I32,
                      _P],
     "hm_attention_plan": [_P, _I32, _I32, _I32, _I32, _P, _P],
+    "hm_set_attention_family": [_I32],
+    "hm_attention_family": [],
     "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
 EPI_STORE, EPI_SWIGLU, EPI_RESIDUAL, EPI_ARGMAX, EPI_F32 = 0, 1, 2, 3, 4
 
 _lib_model = None
 _lock = threading.Lock()
+
+
+ATTENTION_FAMILIES = {"mma_sync": 0, "tcgen05": 1}
+
+
+def set_attention_family(name: str):
+    """Select the attention kernel family for the forwards that follow (process-wide; see hsmodel.h)."""
+    check(lib().hm_set_attention_family(ATTENTION_FAMILIES[name]))
+
+
+def attention_family() -> str:
+    return {v: k for k, v in ATTENTION_FAMILIES.items()}[lib().hm_attention_family()]
 
 
 def lib():

@@ -1,5 +1,5 @@
 """Checks run in a fresh process per attention kernel family (the family is chosen once per process
-from HM_ATTN_TC / HM_ATTN_V2): varlen blocks vs an fp32 reference, one-row-at-a-time invariance,
+from HM_ATTN_MMA / HM_ATTN_W8): varlen blocks vs an fp32 reference, one-row-at-a-time invariance,
 many work items per persistent CTA, and greedy-with-speculation == greedy on the tiny model.
 Used by tests/test_model_gpu.py::test_attention_family_subprocess."""
 import os

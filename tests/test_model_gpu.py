@@ -385,11 +385,11 @@ def test_attention_family_subprocess(family):
     import subprocess
     import sys
     env = dict(os.environ)
-    env.pop("HM_ATTN_TC", None)
     env.pop("HM_ATTN_V2", None)
     env.pop("HM_ATTN_W8", None)
-    if family == "tcgen05":
-        env["HM_ATTN_TC"] = "1"
+    env.pop("HM_ATTN_MMA", None)
+    if family in ("mma_sync", "mma_sync_w8"):
+        env["HM_ATTN_MMA"] = "1"
     if family == "mma_sync_w8":
         env["HM_ATTN_W8"] = "1"
     here = os.path.dirname(os.path.abspath(__file__))
