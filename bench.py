@@ -494,7 +494,7 @@ def run_rollout(args, dist, pk):
         roof = {"kernel": label, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "traffic": None}
     std_cfg = (B, P, T, args.samples) == (1024, 256, 4096, 8) and dist.world == 1
-    roof["traffic"], roof["traffic_source"] = measured_traffic("rollout:" + label, std_cfg)
+    roof["traffic"], roof["traffic_source"] = measured_traffic("rollout:%s:%s" % (label, args.attention), std_cfg)
     roof["peak_source"] = pk["source"] + (" sustained" if roof["unit"] == "TFLOP/s" else "")
     distinct = len({tuple(base.tokens[b, i:i + 4]) for b in range(0, B, S) for i in range(0, T - 4, 7)})
     distinct /= max(1, len(range(0, B, S)) * len(range(0, T - 4, 7)))
