@@ -77,20 +77,26 @@ int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w, int32_t M
                         const int32_t* d_m, hm_stream_t stream);
 
 /* RoPE (rotate-half, table cos/sin [max_pos, hd/2] fp32) on q and k of the fused
- * qkv rows, q -> d_q [M, H, hd]; k, v -> cache[slot][kvh][pos][hd] */
+ * qkv rows, q -> d_q [KVH][M][G][hd] (G = H / KVH: kv-group-major, so a group's
+ * query rows are contiguous -- the attention Q tiles load them as plain 2-D boxes);
+ * k, v -> cache[slot][kvh][pos][hd] */
 int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_row_slot, const float* d_cos,
                       const float* d_sin, int32_t M, int32_t H, int32_t KVH, int32_t hd, void* d_q, void* d_kcache,
                       void* d_vcache, int64_t slot_stride, int32_t max_len, const int32_t* d_m, hm_stream_t stream);
 
 /* K4: causal GQA attention for variable-length query blocks.  Sequence s owns
  * query rows [q_off[s], q_off[s] + q_len[s]) at positions pos0[s] + i and KV
- * slot kv_slot[s]; row i attends cache positions [0, pos0[s] + i]. */
+ * slot kv_slot[s]; row i attends cache positions [0, pos0[s] + i].  d_q is
+ * [KVH][q_rows][G][hd] (hm_rope_kv_append's layout with M = q_rows); d_out is
+ * [rows][H * hd]. */
 int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t hd, int32_t max_len,
-                 float scale, void* d_out, int32_t* d_work /* [n_seq+1] scratch or NULL */,
+                 float scale, void* d_out, int32_t* d_work /* hm_attention_work_size() int32 scratch or NULL */,
                  int32_t work_ready /* d_work already holds hm_attention_plan's output */,
-                 int32_t n_slots /* cache slots, > 0 enables TMA loads */, hm_stream_t stream);
+                 int32_t n_slots /* cache slots, > 0 enables TMA loads */,
+                 int32_t q_rows /* row stride of d_q's kv-group planes (> 0) */,
+                 hm_stream_t stream);
 
 /* Attention kernel family for the forwards that follow (process-wide): 0 = mma.sync m16n8k16
  * (4 warps split each 64-key stage), 1 = tcgen05 (TMEM S/P/O, 128-row tiles, 128-key stages; the
@@ -99,7 +105,10 @@ int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, in
 int hm_set_attention_family(int32_t family);
 int hm_attention_family(void);
 
-/* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent). */
+/* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent): the
+ * per-sequence tile prefix and, for the tcgen05 family, each tile's sequence.  d_work holds
+ * hm_attention_work_size(n_seq, max_q_len, H, KVH) int32 values. */
+int64_t hm_attention_work_size(int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH);
 int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                       int32_t* d_work, hm_stream_t stream);
 

@@ -13,6 +13,7 @@
 // batch composition.
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(128) k_attention(const __nv_bfloat16* __restri
                                                    const __nv_bfloat16* __restrict__ vc, int64_t slot_stride,
                                                    const int32_t* __restrict__ q_off, const int32_t* __restrict__ q_len,
                                                    const int32_t* __restrict__ pos0, const int32_t* __restrict__ kv_slot,
-                                                   int H, int KVH, int max_len, float scale_log2,
+                                                   int H, int KVH, int q_rows, int max_len, float scale_log2,
                                                    __nv_bfloat16* __restrict__ out) {
   constexpr int CH = HD / 8;   // 16-byte chunks per row
   const int tile = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
@@ -94,8 +95,7 @@ __global__ void __launch_bounds__(128) k_attention(const __nv_bfloat16* __restri
     const int rr = tile * AT_ROWS + r;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (rr < rows_total) {
-      const int qi = rr / G, hj = kvh * G + rr % G;
-      v = reinterpret_cast<const uint4*>(q + ((size_t)(qo + qi) * H + hj) * HD)[ch];
+      v = reinterpret_cast<const uint4*>(q + ((size_t)(kvh * q_rows + qo) * G + rr) * HD)[ch];   // [KVH][rows][G][hd]
     }
     sQ[swz<HD>(r, ch)] = v;
   }
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_attention2(const _
                                                     const int32_t* __restrict__ q_len,
                                                     const int32_t* __restrict__ pos0,
                                                     const int32_t* __restrict__ kv_slot, int H, int KVH,
-                                                    int max_len, float scale_log2,
+                                                    int q_rows, int max_len, float scale_log2,
                                                     __nv_bfloat16* __restrict__ out, int n_seq,
                                                     const int32_t* __restrict__ work,
                                                     const __grid_constant__ CUtensorMap tmK,
@@ -319,8 +319,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_attention2(const _
     const int rr = tile * ROWS + r;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (rr < rows_total) {
-      const int qi = rr / G, hj = kvh * G + rr % G;
-      v = reinterpret_cast<const uint4*>(q + ((size_t)(qo + qi) * H + hj) * HD)[ch];
+      v = reinterpret_cast<const uint4*>(q + ((size_t)(kvh * q_rows + qo) * G + rr) * HD)[ch];   // [KVH][rows][G][hd]
     }
     sQ[swz<HD>(r, ch)] = v;
   }
@@ -602,7 +601,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_attention2(const _
 }
 
 // work[s] = sum over earlier sequences of ceil(q_len * G / rows); work[n_seq] = total (single block)
-__global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G, int rows, int32_t* __restrict__ work) {
+// work[s] = first tile of sequence s (exclusive prefix of ceil(q_len * G / rows)), work[n_seq] = total; with
+// tile_seq (tcgen05 family) also tile_seq[t] = the sequence of tile t
+__global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G, int rows, int32_t* __restrict__ work,
+                             int32_t* __restrict__ tile_seq) {
   __shared__ int warp_sums[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -630,6 +632,8 @@ __global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G
     __syncthreads();
     const int off = carry + warp_sums[wid] + incl - t;
     if (s < n_seq) work[s] = off;
+    if (tile_seq)
+      for (int i = 0; i < t; ++i) tile_seq[off + i] = s;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = off + t;
     __syncthreads();
@@ -643,11 +647,12 @@ __global__ void k_attn_tiles(const int32_t* __restrict__ q_len, int n_seq, int G
 // must share one kernel family)
 constexpr int kTcRows = 128;
 constexpr int kTcKeys = 128;   // keys per K/V stage: the TMA box height of the tcgen05 path
+inline int tc_tile_rows(int) { return kTcRows; }
 template <int HD>
 int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
-                   const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
-                   void* d_out, const int32_t* d_work, const CUtensorMap& mk, const CUtensorMap& mv,
-                   const CUtensorMap& mk64, const CUtensorMap& mv64, cudaStream_t st);
+                   const int32_t* d_kv_slot, int32_t n_seq, int32_t H, int32_t KVH, int32_t q_rows, int32_t max_len,
+                   float scale_log2, void* d_out, const int32_t* d_work, const CUtensorMap& mq, const CUtensorMap& mk,
+                   const CUtensorMap& mv, const CUtensorMap& mk64, const CUtensorMap& mv64, cudaStream_t st);
 // attention family: -1 = not chosen yet (environment default), 0 = mma.sync, 1 = tcgen05 (hm_set_attention_family)
 inline int& attn_family() {
   static int family = -1;
@@ -671,7 +676,7 @@ template <int HD, int SL>
 int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, int64_t slot_stride,
                  const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0, const int32_t* d_kv_slot,
                  int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH, int32_t max_len, float scale_log2,
-                 void* d_out, int32_t* d_work, int32_t n_slots, int work_ready, cudaStream_t st) {
+                 void* d_out, int32_t* d_work, int32_t n_slots, int work_ready, int32_t q_rows, cudaStream_t st) {
   constexpr int ROWS = 16 * SL;
   const int ring = 2 * 3 * 64 * HD * 2;                  // K + V stages
   const int merge = 4 * ROWS * HD * 4 + 2 * 4 * ROWS * 4;
@@ -701,7 +706,7 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
     if (!work_ready) {
-      k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work);
+      k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, ROWS, d_work, nullptr);
       hm_count_launches(1);
     }
     if constexpr (SL == 2) {
@@ -718,20 +723,20 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
         }
         k_attention2<HD, 2, 8><<<n_sm * occ8, 256, smem, st>>>(
             (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
-            d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
+            d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
             mk, mv, use_tma, attn_flags());
         return 0;
       }
     }
     k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
-        d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
+        d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
         mk, mv, use_tma, attn_flags());
   } else {
     dim3 grid(KVH, n_seq);
     k_attention2<HD, SL><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                   (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
-                                                  d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                  d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2,
                                                   (__nv_bfloat16*)d_out, n_seq, nullptr, mk, mv, use_tma, attn_flags());
   }
   return 0;
@@ -751,14 +756,22 @@ extern "C" int hm_attention_family(void) { return hm::attn_tc_enabled() ? 1 : 0;
 
 // Work list of the persistent attention kernel, computed once per forward (q_len is the same for
 // every layer): work[s] = first tile of sequence s, work[n_seq] = total tiles.
+extern "C" int64_t hm_attention_work_size(int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH) {
+  if (n_seq <= 0 || max_q_len <= 0 || KVH <= 0 || H % KVH) return 0;
+  const int G = H / KVH;
+  return (int64_t)n_seq + 1 + (int64_t)n_seq * (((int64_t)max_q_len * G + hm::kTcRows - 1) / hm::kTcRows);
+}
+
 extern "C" int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                                  int32_t* d_work, hm_stream_t stream) {
   if (n_seq <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
   const int G = H / KVH;
   // must match the tile height chosen in hm_attention (which re-plans if it cannot take the tcgen05 path)
-  const int rows = hm::attn_tc_enabled() ? hm::kTcRows : (max_q_len * G <= 16 ? 16 : 32);
-  hm::k_attn_tiles<<<1, 1024, 0, (cudaStream_t)stream>>>(d_q_len, n_seq, G, rows, d_work);
+  const bool tc = hm::attn_tc_enabled();
+  const int rows = tc ? hm::tc_tile_rows(G) : (max_q_len * G <= 16 ? 16 : 32);
+  hm::k_attn_tiles<<<1, 1024, 0, (cudaStream_t)stream>>>(d_q_len, n_seq, G, rows, d_work,
+                                                         tc ? d_work + n_seq + 1 : nullptr);
   hm_count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }
@@ -769,32 +782,39 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
                             const int32_t* d_q_off, const int32_t* d_q_len, const int32_t* d_pos0,
                             const int32_t* d_kv_slot, int32_t n_seq, int32_t max_q_len, int32_t H, int32_t KVH,
                             int32_t hd, int32_t max_len, float scale, void* d_out, int32_t* d_work,
-                            int32_t work_ready, int32_t n_slots, hm_stream_t stream) {
+                            int32_t work_ready, int32_t n_slots, int32_t q_rows, hm_stream_t stream) {
   if (n_seq <= 0 || max_q_len <= 0) return HM_OK;
   if (H % KVH) { hm_set_error("H % KVH"); return HM_ERR_INVALID; }
+  if (q_rows <= 0) { hm_set_error("hm_attention: q_rows (row stride of d_q's kv-group planes) must be > 0"); return HM_ERR_INVALID; }
   const int G = H / KVH;
   dim3 grid((max_q_len * G + hm::AT_ROWS - 1) / hm::AT_ROWS, KVH, n_seq);
   const float scale_log2 = scale * 1.4426950408889634f;
   cudaStream_t st = (cudaStream_t)stream;
   if (hm::attn_tc_enabled()) {
-    // tcgen05 path: needs the persistent work list and the cache geometry for the TMA maps
-    CUtensorMap mk, mv, mk64, mv64;   // full 128-key stage boxes and the trimmed last-stage boxes
+    // tcgen05 path: needs the persistent work list and the cache and q geometry for the TMA maps; its packed
+    // item words hold s in 20 bits, the tile in 8 and the kv head in 4
+    if (n_seq >= (1 << 20) || KVH > 16 || ((int64_t)max_q_len * G + hm::kTcRows - 1) / hm::kTcRows > 256) {
+      hm_set_error("hm_attention: n_seq, KVH or max_q_len beyond the tcgen05 kernel's limits");
+      return HM_ERR_INVALID;
+    }
+    CUtensorMap mq, mk, mv, mk64, mv64;   // 16-row Q blocks; 128-key and trimmed 64-key K/V stages
     const int64_t rows = (int64_t)n_slots * KVH * max_len;
     if (d_work && n_slots > 0 && (hd == 128 || hd == 64) &&
+        hm_make_tma_map(&mq, d_q, (int64_t)KVH * q_rows * G, hd, hd, 16) &&
         hm_make_tma_map(&mk, d_kcache, rows, hd, hd, hm::kTcKeys) &&
         hm_make_tma_map(&mv, d_vcache, rows, hd, hd, hm::kTcKeys) &&
         hm_make_tma_map(&mk64, d_kcache, rows, hd, hd, hm::kTcKeys / 2) &&
         hm_make_tma_map(&mv64, d_vcache, rows, hd, hd, hm::kTcKeys / 2)) {
       if (!work_ready) {
-        hm::k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, hm::kTcRows, d_work);
+        hm::k_attn_tiles<<<1, 1024, 0, st>>>(d_q_len, n_seq, G, hm::tc_tile_rows(G), d_work, d_work + n_seq + 1);
         hm_count_launches(1);
       }
       if (hd == 128)
-        hm::launch_attn_tc<128>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
-                                d_work, mk, mv, mk64, mv64, st);
+        hm::launch_attn_tc<128>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, q_rows, max_len, scale_log2, d_out,
+                                d_work, mq, mk, mv, mk64, mv64, st);
       else
-        hm::launch_attn_tc<64>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, max_len, scale_log2, d_out,
-                               d_work, mk, mv, mk64, mv64, st);
+        hm::launch_attn_tc<64>(d_q, d_q_off, d_q_len, d_pos0, d_kv_slot, n_seq, H, KVH, q_rows, max_len, scale_log2, d_out,
+                               d_work, mq, mk, mv, mk64, mv64, st);
       hm_count_launches(1);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) { hm_set_error(cudaGetErrorString(e)); return HM_ERR_CUDA; }
@@ -808,14 +828,14 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     const bool one = max_q_len * G <= 16;
     if (hd == 128) {
       if (one) hm::launch_attn2<128, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
+                                        n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, q_rows, st);
       else hm::launch_attn2<128, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
+                                    n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, q_rows, st);
     } else {
       if (one) hm::launch_attn2<64, 1>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
+                                       n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, q_rows, st);
       else hm::launch_attn2<64, 2>(d_q, d_kcache, d_vcache, slot_stride, d_q_off, d_q_len, d_pos0, d_kv_slot,
-                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, st);
+                                   n_seq, max_q_len, H, KVH, max_len, scale_log2, d_out, d_work, n_slots, work_ready, q_rows, st);
     }
   } else if (hd == 128) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 128 * 2;
@@ -823,13 +843,13 @@ extern "C" int hm_attention(const void* d_q, const void* d_kcache, const void* d
     if (!set) { cudaFuncSetAttribute(hm::k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set = true; }
     hm::k_attention<128><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                   (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
-                                                  d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                  d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2,
                                                   (__nv_bfloat16*)d_out);
   } else if (hd == 64) {
     const int smem = (hm::AT_ROWS + 4 * hm::AT_KEYS) * 64 * 2;
     hm::k_attention<64><<<grid, 128, smem, st>>>((const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache,
                                                  (const __nv_bfloat16*)d_vcache, slot_stride, d_q_off, d_q_len,
-                                                 d_pos0, d_kv_slot, H, KVH, max_len, scale_log2,
+                                                 d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2,
                                                  (__nv_bfloat16*)d_out);
   } else {
     hm_set_error("attention: head dim must be 64 or 128");

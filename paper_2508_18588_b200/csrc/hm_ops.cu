@@ -135,6 +135,7 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* 
   const float* c = cosb + (size_t)p * half;
   const float* s = sinb + (size_t)p * half;
   const int n_rot = (H + KVH) * hc;
+  const int G = H / KVH;
   for (int t = threadIdx.x; t < n_rot + KVH * 2 * hc; t += blockDim.x) {
     if (t < n_rot) {
       const int head = t / hc, i = (t % hc) * 8;
@@ -157,7 +158,7 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* 
         rb2[e] = __floats2bfloat162_rn(b.x * cc[2 * e] + a.x * ss[2 * e], b.y * cc[2 * e + 1] + a.y * ss[2 * e + 1]);
       }
       __nv_bfloat16* dst;
-      if (head < H) dst = q + ((size_t)row * H + head) * hd;
+      if (head < H) dst = q + (((size_t)(head / G) * M + row) * G + head % G) * hd;   // [KVH][M][G][hd]
       else dst = kc + (size_t)slot * slot_stride + ((size_t)(head - H) * max_len + p) * hd;
       *reinterpret_cast<uint4*>(dst + i) = ra;
       *reinterpret_cast<uint4*>(dst + i + half) = rb;

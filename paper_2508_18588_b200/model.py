@@ -38,8 +38,9 @@ SIGNATURES = {
     "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
     "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _I32,
-                     _P],
+                     _I32, _P],
     "hm_attention_plan": [_P, _I32, _I32, _I32, _I32, _P, _P],
+    "hm_attention_work_size": [_I32, _I32, _I32, _I32],
     "hm_set_attention_family": [_I32],
     "hm_attention_family": [],
     "hm_build_verify_batch": [_I32, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -73,8 +74,8 @@ def lib():
                 fn = getattr(L, name)
                 if name == "hm_last_error":
                     fn.restype, fn.argtypes = ctypes.c_char_p, []
-                elif name == "hm_launch_count":
-                    fn.restype, fn.argtypes = ctypes.c_int64, []
+                elif name in ("hm_launch_count", "hm_attention_work_size"):
+                    fn.restype, fn.argtypes = ctypes.c_int64, argt or []
                 else:
                     fn.restype, fn.argtypes = ctypes.c_int, argt
             _lib_model = L
@@ -226,14 +227,15 @@ class Forward:
         self.y = torch.empty((M, d), dtype=torch.float32, device=device)   # O/down-proj output, added in the norm
         self.h = torch.empty((M, d), **bf)
         self.qkv = torch.empty((M, cfg.qkv_dim), **bf)
-        self.q = torch.empty((M, cfg.n_heads, cfg.head_dim), **bf)
+        self.q = torch.empty((M, cfg.n_heads, cfg.head_dim), **bf)   # used as [KVH][rows][G][hd] (hm_rope_kv_append)
         self.attn = torch.empty((M, cfg.n_heads * cfg.head_dim), **bf)
         self.act = torch.empty((M, cfg.ffn), **bf)
         self.n_tiles = cfg.vocab // 128
         self.amax_val = torch.empty((M, self.n_tiles), dtype=torch.float32, device=device)
         self.amax_idx = torch.empty((M, self.n_tiles), dtype=torch.int32, device=device)
         self.argmax = torch.empty(M, dtype=torch.int32, device=device)
-        self.attn_work = torch.empty(M + 1, dtype=torch.int32, device=device)   # attention work-list prefix
+        # attention work list (tile prefix + tile -> sequence map), grown on demand outside graph capture
+        self.attn_work = torch.empty(2 * M + 2, dtype=torch.int32, device=device)
         self.cos, self.sin = w.rope_tables(cache.max_len + 64, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self.temperature = 0.0   # 0 = greedy argmax; > 0 = Gumbel-max sampling (hm_lm_head_sample)
@@ -250,6 +252,11 @@ class Forward:
             raise ValueError(f"{M} rows > max_rows {self.max_rows}")
         L = lib()
         cfg, w = self.cfg, self.w
+        need = L.hm_attention_work_size(n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads)
+        if need > self.attn_work.numel():
+            if torch.cuda.is_current_stream_capturing():
+                raise ValueError(f"attention work list needs {need} entries: run once before capturing")
+            self.attn_work = torch.empty(need, dtype=torch.int32, device=self.device)
         s_obj = stream or torch.cuda.current_stream(self.device)
         st = s_obj.cuda_stream
         mp = m_dev.data_ptr() if m_dev is not None else None
@@ -289,7 +296,7 @@ class Forward:
                                                   kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
                                                   self.attn.data_ptr(), self.attn_work.data_ptr(), 1,
-                                                  self.cache.n_slots, st))
+                                                  self.cache.n_slots, M, st))
             k("gemm_o", lambda: L.hm_gemm(EPI_F32, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
                                           M, d, hd_all, None, None, 0, y, d, None, None, mp, st))
             k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, layer["ln2"].data_ptr(), M, d, cfg.eps,

@@ -12,14 +12,21 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2508_18588_b200.model as Mo  # noqa: E402
 
 
+def _kv_major(q, KVH):
+    """[rows, H, hd] -> the kernels' kv-group-major [KVH][rows][G][hd] layout (hm_rope_kv_append's)."""
+    M, H, hd = q.shape
+    return q.view(M, KVH, H // KVH, hd).transpose(0, 1).contiguous()
+
+
+
 def attn(q, kc, vc, seqs, H, KVH, hd, max_len, slots, work, M):
     i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
     out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
     meta = [i32([s[j] for s in seqs]) for j in range(4)]
-    Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+    Mo.check(Mo.lib().hm_attention(_kv_major(q, KVH).data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
                                    meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(), meta[3].data_ptr(),
                                    len(seqs), max(s[1] for s in seqs), H, KVH, hd, max_len, 1.0 / np.sqrt(hd),
-                                   out.data_ptr(), work.data_ptr(), 0, slots, 0))
+                                   out.data_ptr(), work.data_ptr(), 0, slots, M, 0))
     torch.cuda.synchronize()
     return out.view(M, H, hd)
 
@@ -37,7 +44,7 @@ def main():
         pos0 = rng.integers(0, max_len - 34, size=n)
         M = int(q_len.sum())
         q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
-        work = torch.empty(M + 1, dtype=torch.int32, device="cuda")
+        work = torch.empty(2 * M + 2, dtype=torch.int32, device="cuda")   # >= hm_attention_work_size
         seqs = [(int(q_off[s]), int(q_len[s]), int(pos0[s]), s) for s in range(n)]
         out = attn(q, kc, vc, seqs, H, KVH, hd, max_len, n, work, M)
         # fp32 reference on a sample of rows

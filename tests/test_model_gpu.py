@@ -10,6 +10,13 @@ is required wherever the reference top-2 margin exceeds that bound.
 import numpy as np
 import pytest
 
+
+def _kv_major(q, KVH):
+    """[rows, H, hd] -> the kernels' kv-group-major [KVH][rows][G][hd] layout (hm_rope_kv_append's)."""
+    M, H, hd = q.shape
+    return q.view(M, KVH, H // KVH, hd).transpose(0, 1).contiguous()
+
+
 pytestmark = pytest.mark.gpu
 
 
@@ -152,11 +159,11 @@ def test_attention_varlen_and_invariance(torch, H, KVH, hd):
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
         out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
         meta = [i32([s[j] for s in sq]) for j in range(4)]   # keep alive across the launch
-        Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+        Mo.check(Mo.lib().hm_attention(_kv_major(q, KVH).data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
                                        meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                        meta[3].data_ptr(), len(sq), max(s[1] for s in sq), H, KVH, hd, max_len,
                                        1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
-                                       0, slots if tma else 0, 0))
+                                       0, slots if tma else 0, M, 0))
         torch.cuda.synchronize()
         return out.view(M, H, hd)
 
@@ -189,17 +196,17 @@ def test_attention_many_items_per_cta(torch):
     pos0 = rng.integers(0, max_len - 34, size=n)
     M = int(q_len.sum())
     q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
-    work = torch.empty(M + 1, dtype=torch.int32, device="cuda")   # [n_seq + 1] for the decode run below
+    work = torch.empty(2 * M + 2, dtype=torch.int32, device="cuda")   # hm_attention_work_size for the decode run below
     i32 = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32)).cuda()  # noqa: E731
 
     def run(qo, ql, p0, sl, persistent):
         out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
         meta = [i32(qo), i32(ql), i32(p0), i32(sl)]
-        Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+        Mo.check(Mo.lib().hm_attention(_kv_major(q, KVH).data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
                                        meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                        meta[3].data_ptr(), len(ql), int(max(ql)), H, KVH, hd, max_len,
                                        1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
-                                       0, slots, 0))
+                                       0, slots, M, 0))
         torch.cuda.synchronize()
         return out
 

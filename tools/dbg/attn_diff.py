@@ -14,16 +14,16 @@ q_off = np.concatenate([[0], np.cumsum(q_len)[:-1]])
 pos0 = rng.integers(0, max_len - 34, size=n)
 M = int(q_len.sum())
 q = torch.randn(M, H, hd, device="cuda", generator=g).to(torch.bfloat16)
-work = torch.empty(M + 1, dtype=torch.int32, device="cuda")
+work = torch.empty(2 * M + 2, dtype=torch.int32, device="cuda")
 i32 = lambda v: torch.as_tensor(np.asarray(v, dtype=np.int32)).cuda()
 def run(qo, ql, p0, sl, persistent):
     out = torch.zeros(M, H * hd, dtype=torch.bfloat16, device="cuda")
     meta = [i32(qo), i32(ql), i32(p0), i32(sl)]
-    Mo.check(Mo.lib().hm_attention(q.data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
+    Mo.check(Mo.lib().hm_attention(_kv_major(q, KVH).data_ptr(), kc.data_ptr(), vc.data_ptr(), KVH * max_len * hd,
                                    meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
                                    meta[3].data_ptr(), len(ql), int(max(ql)), H, KVH, hd, max_len,
                                    1.0 / np.sqrt(hd), out.data_ptr(), work.data_ptr() if persistent else None,
-                                   0, slots, 0))
+                                   0, slots, M, 0))
     torch.cuda.synchronize()
     return out.view(M, H, hd).float()
 slot = np.arange(n)
@@ -36,6 +36,13 @@ rows, heads = torch.nonzero(bad.any(-1), as_tuple=True)
 seq_of_row = np.repeat(np.arange(n), q_len)
 print("bad (row, head) pairs", len(rows))
 import collections
+
+
+def _kv_major(q, KVH):
+    """[rows, H, hd] -> the kernels' kv-group-major [KVH][rows][G][hd] layout (hm_rope_kv_append's)."""
+    M, H, hd = q.shape
+    return q.view(M, KVH, H // KVH, hd).transpose(0, 1).contiguous()
+
 byseq = collections.Counter()
 for r, h in zip(rows.tolist()[:2000], heads.tolist()[:2000]):
     s = seq_of_row[r]
