@@ -84,6 +84,16 @@ int hm_rope_kv_append(const void* d_qkv, const int32_t* d_pos, const int32_t* d_
                       const float* d_sin, int32_t M, int32_t H, int32_t KVH, int32_t hd, void* d_q, void* d_kcache,
                       void* d_vcache, int64_t slot_stride, int32_t max_len, const int32_t* d_m, hm_stream_t stream);
 
+/* K3 + K5 fused: qkv = X . Wqkv^T + bias (rounded to bf16 as hm_gemm would store it), then RoPE on the q
+ * and k heads at d_pos[row] and the hm_rope_kv_append writes -- q kv-group-major into d_q with M = q_rows,
+ * k and v into cache[d_row_slot[row]][kvh][pos] -- from the GEMM epilogue: the qkv activations never
+ * reach HBM.  Same bits as hm_gemm(HM_EPI_STORE) followed by hm_rope_kv_append. */
+int hm_gemm_qkv_rope(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t K,
+                     const void* d_bias, int32_t H, int32_t KVH, int32_t hd, const int32_t* d_pos,
+                     const int32_t* d_row_slot, const float* d_cos, const float* d_sin, void* d_q, int32_t q_rows,
+                     void* d_kcache, void* d_vcache, int64_t slot_stride, int32_t max_len, const int32_t* d_m,
+                     hm_stream_t stream);
+
 /* K4: causal GQA attention for variable-length query blocks.  Sequence s owns
  * query rows [q_off[s], q_off[s] + q_len[s]) at positions pos0[s] + i and KV
  * slot kv_slot[s]; row i attends cache positions [0, pos0[s] + i].  d_q is

@@ -40,7 +40,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;           // 64 bf16 = 128 B = one swizzle row
 constexpr int kThreads = 192;    // 6 warps
 
-enum { EPI_STORE = 0, EPI_SWIGLU = 1, EPI_RESIDUAL = 2, EPI_ARGMAX = 3, EPI_F32 = 4 };
+enum { EPI_STORE = 0, EPI_SWIGLU = 1, EPI_RESIDUAL = 2, EPI_ARGMAX = 3, EPI_F32 = 4, EPI_ROPE = 5 };
 
 struct EpiParams {
   int M, N, K;
@@ -58,7 +58,23 @@ struct EpiParams {
   const int* key1;
   unsigned long long seed;
   float inv_temp;
+  // ROPE (fused QKV projection + RoPE + KV append): columns are H q heads, KVH k heads, KVH v heads of hd
+  const int* pos;              // [M] position of each row
+  const int* row_slot;         // [M] KV-cache slot of each row
+  const float* cos_t;          // [max_pos, hd/2]
+  const float* sin_t;
+  __nv_bfloat16* q_out;        // [KVH][ldq rows][G][hd]
+  __nv_bfloat16* kcache;       // [slot][KVH][max_len][hd]
+  __nv_bfloat16* vcache;
+  long long slot_stride;
+  int H, KVH, hd, max_len, ldq;
 };
+
+// rotate-half RoPE pair, rounding pinned (hm_rope_kv_append computes the same bits)
+__device__ __forceinline__ void rope_pair(float a, float b, float c, float s, float& ra, float& rb) {
+  ra = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
+  rb = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
+}
 
 // Counter-based hash RNG for Gumbel-max sampling: the noise of vocabulary entry v
 // at (seed, sequence, position) is a pure function of those four integers, so a
@@ -94,6 +110,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// v[i] += bias[i], i < 32 (16-byte loads; the same fp32 adds as element-wise)
+__device__ __forceinline__ void add_bias32(float* v, const __nv_bfloat16* bias) {
+  const uint4* b4 = reinterpret_cast<const uint4*>(bias);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 w = b4[j];
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&u[e]);
+      v[8 * j + 2 * e] += __low2float(h);
+      v[8 * j + 2 * e + 1] += __high2float(h);
+    }
+  }
+}
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst_, const float* v) {
   uint4* dst = reinterpret_cast<uint4*>(dst_);
 #pragma unroll
@@ -213,10 +244,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
           float v[32];
           tmem_ld32(t_row + c, v);
           const int col0 = n_blk * BN + c;
-          if (p.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += __bfloat162float(p.bias[col0 + i]);
-          }
+          if (p.bias) add_bias32(v, p.bias + col0);
           if (live) {
             if constexpr (EPI == EPI_STORE) {
               store_bf16x32(p.out + (size_t)row * p.ldo + col0, v);
@@ -236,6 +264,60 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
                 r.w += v[4 * i + 3];
                 dst[i] = r;
               }
+            }
+          }
+        }
+      } else if constexpr (EPI == EPI_ROPE) {
+        // q/k/v heads of this tile: bias, round to bf16 (the unfused path's qkv activations), rotate q and
+        // k at the row's position, write q kv-group-major and k, v into the cache
+        const int hd = p.hd, half = hd / 2, G = p.H / p.KVH;
+        const int pos = live ? p.pos[row] : 0;
+        const long long slot = live ? p.row_slot[row] : 0;
+#pragma unroll 1
+        for (int hc = 0; hc < cmax; hc += hd) {
+          const int head = (n_blk * BN + hc) / hd;   // 0..H+2KVH-1
+          __nv_bfloat16* dst;
+          if (head < p.H)
+            dst = p.q_out + (((size_t)(head / G) * p.ldq + row) * G + head % G) * hd;
+          else if (head < p.H + p.KVH)
+            dst = p.kcache + slot * p.slot_stride + ((size_t)(head - p.H) * p.max_len + pos) * hd;
+          else
+            dst = p.vcache + slot * p.slot_stride + ((size_t)(head - p.H - p.KVH) * p.max_len + pos) * hd;
+          const bool rot = head < p.H + p.KVH;
+#pragma unroll 1
+          for (int c = 0; c < half; c += 32) {
+            float a[32], b[32];
+            tmem_ld32(t_row + hc + c, a);
+            tmem_ld32(t_row + hc + half + c, b);
+            const int col = n_blk * BN + hc + c;
+            if (p.bias) {
+              add_bias32(a, p.bias + col);
+              add_bias32(b, p.bias + col + half);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              a[i] = __bfloat162float(__float2bfloat16_rn(a[i]));
+              b[i] = __bfloat162float(__float2bfloat16_rn(b[i]));
+            }
+            if (rot && live) {
+              const float4* cs = reinterpret_cast<const float4*>(p.cos_t + (size_t)pos * half + c);
+              const float4* sn = reinterpret_cast<const float4*>(p.sin_t + (size_t)pos * half + c);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 c4 = cs[j], s4 = sn[j];
+                const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float ra, rb;
+                  rope_pair(a[4 * j + e], b[4 * j + e], cc[e], ss[e], ra, rb);
+                  a[4 * j + e] = ra;
+                  b[4 * j + e] = rb;
+                }
+              }
+            }
+            if (live) {
+              store_bf16x32(dst + c, a);
+              store_bf16x32(dst + half + c, b);
             }
           }
         }
@@ -400,7 +482,8 @@ extern "C" int hm_gemm_bn(int32_t n) {
 static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
                      int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
                      float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, const int32_t* key0,
-                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream);
+                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream,
+                     const hm::EpiParams* rope = nullptr);
 
 extern "C" int hm_gemm(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
                        int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
@@ -424,7 +507,8 @@ extern "C" int hm_lm_head_sample(const void* d_x, int64_t ldx, const void* d_w, 
 static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N,
                      int32_t K, const void* d_bias, void* d_out, int64_t ldo, float* d_resid, int64_t ldr,
                      float* d_amax_val, int32_t* d_amax_idx, const int32_t* d_m, const int32_t* key0,
-                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream) {
+                     const int32_t* key1, uint64_t seed, float inv_temp, hm_stream_t stream,
+                     const hm::EpiParams* rope) {
   if (M <= 0) return HM_OK;
   if (K % hm::BK != 0 || N % 128 != 0) {
     hm_set_error("hm_gemm: K must be a multiple of 64 and N of 128");
@@ -441,7 +525,8 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   static const int narrow_off = getenv("HM_GEMM_NO_NARROW") != nullptr;   // A/B switch for profiling only
-  if (BN == 256 && !narrow_off && (epi == HM_EPI_STORE || epi == HM_EPI_F32 || epi == HM_EPI_RESIDUAL) &&
+  if (BN == 256 && !narrow_off &&
+      (epi == HM_EPI_STORE || epi == HM_EPI_F32 || epi == HM_EPI_RESIDUAL || epi == hm::EPI_ROPE) &&
       ((M + hm::BM - 1) / hm::BM) * ((N + 255) / 256) < g_num_sms)
     BN = 128;
   if (epi == HM_EPI_SWIGLU && N % BN != 0) {
@@ -454,6 +539,7 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
     return HM_ERR_INVALID;
   }
   hm::EpiParams p{};
+  if (rope) p = *rope;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -478,6 +564,7 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
       case HM_EPI_RESIDUAL: return launch<256, 4, hm::EPI_RESIDUAL>(mx, mw, p, st);
       case HM_EPI_F32: return launch<256, 4, hm::EPI_F32>(mx, mw, p, st);
       case HM_EPI_ARGMAX: return launch<256, 4, hm::EPI_ARGMAX>(mx, mw, p, st);
+      case hm::EPI_ROPE: return launch<256, 4, hm::EPI_ROPE>(mx, mw, p, st);
     }
   } else {
     switch (epi) {
@@ -486,10 +573,39 @@ static int gemm_impl(int32_t epi, const void* d_x, int64_t ldx, const void* d_w,
       case HM_EPI_RESIDUAL: return launch<128, 6, hm::EPI_RESIDUAL>(mx, mw, p, st);
       case HM_EPI_F32: return launch<128, 6, hm::EPI_F32>(mx, mw, p, st);
       case HM_EPI_ARGMAX: return launch<128, 6, hm::EPI_ARGMAX>(mx, mw, p, st);
+      case hm::EPI_ROPE: return launch<128, 6, hm::EPI_ROPE>(mx, mw, p, st);
     }
   }
   hm_set_error("unknown epilogue");
   return HM_ERR_INVALID;
+}
+
+extern "C" int hm_gemm_qkv_rope(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t K,
+                                const void* d_bias, int32_t H, int32_t KVH, int32_t hd, const int32_t* d_pos,
+                                const int32_t* d_row_slot, const float* d_cos, const float* d_sin, void* d_q,
+                                int32_t q_rows, void* d_kcache, void* d_vcache, int64_t slot_stride,
+                                int32_t max_len, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (KVH <= 0 || H % KVH || (hd != 64 && hd != 128) || q_rows < M) {
+    hm_set_error("hm_gemm_qkv_rope: H % KVH, hd in {64, 128} and q_rows >= M required");
+    return HM_ERR_INVALID;
+  }
+  hm::EpiParams r{};
+  r.pos = d_pos;
+  r.row_slot = d_row_slot;
+  r.cos_t = d_cos;
+  r.sin_t = d_sin;
+  r.q_out = static_cast<__nv_bfloat16*>(d_q);
+  r.kcache = static_cast<__nv_bfloat16*>(d_kcache);
+  r.vcache = static_cast<__nv_bfloat16*>(d_vcache);
+  r.slot_stride = slot_stride;
+  r.H = H;
+  r.KVH = KVH;
+  r.hd = hd;
+  r.max_len = max_len;
+  r.ldq = q_rows;
+  return gemm_impl(hm::EPI_ROPE, d_x, ldx, d_w, ldw, M, (H + 2 * KVH) * hd, K, d_bias, nullptr, 0, nullptr, 0,
+                   nullptr, nullptr, d_m, nullptr, nullptr, 0, 0.f, stream, &r);
 }
 
 extern "C" int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles,

@@ -154,8 +154,11 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* 
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 a = __bfloat1622float2(a2[e]), b = __bfloat1622float2(b2[e]);
-        ra2[e] = __floats2bfloat162_rn(a.x * cc[2 * e] - b.x * ss[2 * e], a.y * cc[2 * e + 1] - b.y * ss[2 * e + 1]);
-        rb2[e] = __floats2bfloat162_rn(b.x * cc[2 * e] + a.x * ss[2 * e], b.y * cc[2 * e + 1] + a.y * ss[2 * e + 1]);
+        // rounding pinned: the fused QKV + RoPE GEMM epilogue (hm_gemm_qkv_rope) computes the same bits
+        ra2[e] = __floats2bfloat162_rn(__fsub_rn(__fmul_rn(a.x, cc[2 * e]), __fmul_rn(b.x, ss[2 * e])),
+                                       __fsub_rn(__fmul_rn(a.y, cc[2 * e + 1]), __fmul_rn(b.y, ss[2 * e + 1])));
+        rb2[e] = __floats2bfloat162_rn(__fadd_rn(__fmul_rn(b.x, cc[2 * e]), __fmul_rn(a.x, ss[2 * e])),
+                                       __fadd_rn(__fmul_rn(b.y, cc[2 * e + 1]), __fmul_rn(a.y, ss[2 * e + 1])));
       }
       __nv_bfloat16* dst;
       if (head < H) dst = q + (((size_t)(head / G) * M + row) * G + head % G) * hd;   // [KVH][M][G][hd]

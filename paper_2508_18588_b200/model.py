@@ -37,6 +37,8 @@ SIGNATURES = {
     "hm_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rmsnorm_residual": [_P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P, _P],
+    "hm_gemm_qkv_rope": [_P, _I64, _P, _I64, _I32, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P,
+                         _I64, _I32, _P, _P],
     "hm_attention": [_P, _P, _P, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _F32, _P, _P, _I32, _I32,
                      _I32, _P],
     "hm_attention_plan": [_P, _I32, _I32, _I32, _I32, _P, _P],
@@ -239,6 +241,7 @@ class Forward:
         self.cos, self.sin = w.rope_tables(cache.max_len + 64, device)
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self.temperature = 0.0   # 0 = greedy argmax; > 0 = Gumbel-max sampling (hm_lm_head_sample)
+        self.fused_qkv_rope = True   # False: hm_gemm + hm_rope_kv_append (tests compare the two)
         self.seed = 0
 
     def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
@@ -284,13 +287,20 @@ class Forward:
             yp = None if li == 0 else y
             k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yp, layer["ln1"].data_ptr(), M, d,
                                                        cfg.eps, self.h.data_ptr(), mp, st))
-            k("gemm_qkv", lambda: L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M,
-                                            cfg.qkv_dim, d, layer["bqkv"].data_ptr(), self.qkv.data_ptr(),
-                                            cfg.qkv_dim, None, 0, None, None, mp, st))
-            k("rope_kv", lambda: L.hm_rope_kv_append(self.qkv.data_ptr(), pos.data_ptr(), row_slot.data_ptr(),
-                                                     self.cos.data_ptr(), self.sin.data_ptr(), M, cfg.n_heads,
-                                                     cfg.n_kv_heads, cfg.head_dim, self.q.data_ptr(), kc, vc,
-                                                     self.cache.slot_stride, self.cache.max_len, mp, st))
+            if self.fused_qkv_rope:   # QKV projection, RoPE and the KV append in one kernel (same bits)
+                k("gemm_qkv", lambda: L.hm_gemm_qkv_rope(
+                    self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M, d, layer["bqkv"].data_ptr(), cfg.n_heads,
+                    cfg.n_kv_heads, cfg.head_dim, pos.data_ptr(), row_slot.data_ptr(), self.cos.data_ptr(),
+                    self.sin.data_ptr(), self.q.data_ptr(), M, kc, vc, self.cache.slot_stride, self.cache.max_len,
+                    mp, st))
+            else:
+                k("gemm_qkv", lambda: L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M,
+                                                cfg.qkv_dim, d, layer["bqkv"].data_ptr(), self.qkv.data_ptr(),
+                                                cfg.qkv_dim, None, 0, None, None, mp, st))
+                k("rope_kv", lambda: L.hm_rope_kv_append(self.qkv.data_ptr(), pos.data_ptr(), row_slot.data_ptr(),
+                                                         self.cos.data_ptr(), self.sin.data_ptr(), M, cfg.n_heads,
+                                                         cfg.n_kv_heads, cfg.head_dim, self.q.data_ptr(), kc, vc,
+                                                         self.cache.slot_stride, self.cache.max_len, mp, st))
             k("attention", lambda: L.hm_attention(self.q.data_ptr(), kc, vc, self.cache.slot_stride,
                                                   q_off.data_ptr(), q_len.data_ptr(), pos0.data_ptr(),
                                                   kv_slot.data_ptr(), n_seq, max_q_len, cfg.n_heads,
