@@ -242,6 +242,9 @@ class Forward:
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
         self.temperature = 0.0   # 0 = greedy argmax; > 0 = Gumbel-max sampling (hm_lm_head_sample)
         self.fused_qkv_rope = True   # False: hm_gemm + hm_rope_kv_append (tests compare the two)
+        # True: the O and down projections add into the residual stream in their epilogues (HM_EPI_RESIDUAL)
+        # and the norms that follow read x alone; False: they store fp32 and the next norm adds (same bits)
+        self.residual_in_gemm = os.environ.get("HM_RESIDUAL_IN_GEMM", "0") == "1"
         self.seed = 0
 
     def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
@@ -284,7 +287,7 @@ class Forward:
         for li, layer in enumerate(w.layers):
             kc, vc = self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr()
             # x += y (previous down-proj; none before layer 0), h = rmsnorm(x)
-            yp = None if li == 0 else y
+            yp = None if (li == 0 or self.residual_in_gemm) else y
             k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yp, layer["ln1"].data_ptr(), M, d,
                                                        cfg.eps, self.h.data_ptr(), mp, st))
             if self.fused_qkv_rope:   # QKV projection, RoPE and the KV append in one kernel (same bits)
@@ -307,17 +310,18 @@ class Forward:
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
                                                   self.attn.data_ptr(), self.attn_work.data_ptr(), 1,
                                                   self.cache.n_slots, M, st))
-            k("gemm_o", lambda: L.hm_gemm(EPI_F32, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
-                                          M, d, hd_all, None, None, 0, y, d, None, None, mp, st))
-            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, layer["ln2"].data_ptr(), M, d, cfg.eps,
-                                                       self.h.data_ptr(), mp, st))
+            epi_r, y_r, y_n = (EPI_RESIDUAL, self.x.data_ptr(), None) if self.residual_in_gemm else (EPI_F32, y, y)
+            k("gemm_o", lambda: L.hm_gemm(epi_r, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
+                                          M, d, hd_all, None, None, 0, y_r, d, None, None, mp, st))
+            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y_n, layer["ln2"].data_ptr(), M, d,
+                                                       cfg.eps, self.h.data_ptr(), mp, st))
             k("gemm_gate_up", lambda: L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M,
                                                 2 * cfg.ffn, d, None, self.act.data_ptr(), cfg.ffn, None, 0, None,
                                                 None, mp, st))
-            k("gemm_down", lambda: L.hm_gemm(EPI_F32, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
-                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y, d, None, None, mp, st))
-        k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y, w.final_ln.data_ptr(), M, d, cfg.eps,
-                                                   self.h.data_ptr(), mp, st))
+            k("gemm_down", lambda: L.hm_gemm(epi_r, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
+                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y_r, d, None, None, mp, st))
+        k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), None if self.residual_in_gemm else y,
+                                                   w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
         if logits_out is not None:
             check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
                             logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))

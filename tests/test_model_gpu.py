@@ -249,7 +249,8 @@ def test_tiny_forward_logits_vs_reference(torch):
 @pytest.mark.parametrize("cfg_name", ["TINY", "QWEN25_1P5B"])
 def test_fused_qkv_rope_matches_unfused(torch, cfg_name):
     """hm_gemm_qkv_rope (QKV GEMM + RoPE + KV append in one epilogue) writes the same bits as hm_gemm followed
-    by hm_rope_kv_append: logits, argmax and both KV caches, on a ragged two-sequence batch."""
+    by hm_rope_kv_append, and the residual add in the O / down epilogues the same bits as in the next norm:
+    logits, argmax and both KV caches, on a ragged two-sequence batch."""
     import paper_2508_18588_b200.model as Mo
     cfg = getattr(Mo, cfg_name)
     if cfg_name != "TINY":
@@ -263,17 +264,19 @@ def test_fused_qkv_rope_matches_unfused(torch, cfg_name):
     pos = np.concatenate([np.arange(s, s + n) for s, n in zip(starts, lens)])
     slot = np.concatenate([np.full(n, i) for i, n in enumerate(lens)])
     outs = []
-    for fused in (True, False):
+    for fused, resid in ((True, False), (False, False), (True, True)):
         cache = Mo.KVCache(cfg, 2, 160, "cuda")
         f = Mo.Forward(w, cache, 64, "cuda")
         f.fused_qkv_rope = fused
+        f.residual_in_gemm = resid   # residual add in the O / down GEMM epilogues: the same fp32 adds
         logits = torch.empty(T, cfg.vocab, dtype=torch.bfloat16, device="cuda")
         am = f.run(T, i32(toks), i32(pos), i32(slot), i32([0, lens[0]]), i32(lens), i32(starts), i32([0, 1]), 2,
                    max(lens), logits_out=logits)
         torch.cuda.synchronize()
         outs.append((logits.clone(), am.clone(), cache.k(0).clone(), cache.v(cfg.n_layers - 1).clone()))
-    for a, b in zip(*outs):
-        assert torch.equal(a, b)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
 
 
 def test_tiny_engine_spec_equals_greedy_and_reference_replay(torch):
