@@ -130,6 +130,10 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int
 #define WD_NOTE(id, gs) do { } while (0)
 #endif
 
+#ifndef HM_TC_BACKOFF_NS
+#define HM_TC_BACKOFF_NS 64   // producer back-off when every ring is full
+#endif
+
 #ifdef HM_TC_TRACE
 // debugging aid: clock64 per (event, stage) of CTA 0, read back with hm_debug_attn_trace
 __device__ long long g_tc_trace[16 * 512];
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
           vmore = advance(cv);
         }
       }
-      if (ck.g + cv.g + kq == issued) __nanosleep(64);   // rings full: back off (shares an SMSP with softmax warps)
+      if (ck.g + cv.g + kq == issued) __nanosleep(HM_TC_BACKOFF_NS);   // rings full: back off (shares an SMSP with softmax warps)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (the whole warp walks the items; lane 0 issues)
