@@ -51,3 +51,15 @@ def test_gpu_path_fails_loudly_without_cuda():
     from paper_2508_18588_b200.history import build_tree, Response
     with pytest.raises(RuntimeError):
         build_tree("p", 1, [Response("p", 1, [1, 2, 3], 1.0)])
+
+
+def test_attention_work_size_host_only():
+    """hm_attention_work_size is host arithmetic (no GPU): tile prefix (n_seq + 1) plus one entry per
+    128-row tcgen05 tile of every sequence; invalid shapes return 0."""
+    from paper_2508_18588_b200 import model as Mo
+    L = Mo.lib()
+    assert L.hm_attention_work_size(1024, 33, 12, 2) == 1025 + 1024 * 2    # 33 queries x 6 heads = 198 rows
+    assert L.hm_attention_work_size(1024, 21, 12, 2) == 1025 + 1024        # 126 rows fit one tile
+    assert L.hm_attention_work_size(5, 1, 4, 4) == 6 + 5
+    assert L.hm_attention_work_size(0, 1, 12, 2) == 0
+    assert L.hm_attention_work_size(8, 4, 12, 5) == 0                      # H % KVH != 0
