@@ -72,6 +72,12 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {   // zero-fills if !valid
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -188,7 +194,11 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     for (int i = 0; i < 2; ++i) {
       mbar_init(&m_ready[i], 4);
       mbar_init(&l_ready[i], 4);
+#ifdef HM_TC_QCPASYNC
+      mbar_init(&q_full[i], 4);
+#else
       mbar_init(&q_full[i], 1);
+#endif
       mbar_init(&q_empty[i], 1);
       mbar_init(&o_ready[i], 1);
     }
@@ -310,7 +320,11 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     };
     // Q tiles: item kq's tile goes into buffer kq & 1 once item kq - 2's S products are done; one 16-row
     // box per block (rows past the tile's read the next rows of d_q or zeros past its end: masked padding)
+#ifdef HM_TC_QCPASYNC   // A/B variant: set 0 copies Q with cp.async (softmax section)
+    int kq = n_mine;
+#else
     int kq = 0;
+#endif
     Tab tq;
     fill(tq, 0);
     auto load_q = [&]() {
@@ -472,9 +486,41 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
     Item cur, nxt;
     if (n_mine > 0) cur = item_info(0);
     if (n_mine > 1) nxt = item_info(1);
+#ifdef HM_TC_QCPASYNC
+    // set 0 copies this thread's Q row (tile row of TMEM lane tl) of an item into its tile with cp.async;
+    // q_ready hands the tile over once the copies have landed
+    auto load_q = [&](const Item& x, int qbuf) {
+      const int r = row_of(lane >> 4, lane & 15);
+      const bool lv = r < tile_rows(x.qlen, x.tile);
+      const __nv_bfloat16* src = q + ((size_t)(x.kvh * q_rows + x.qo) * G + x.tile * ROWS + (lv ? r : 0)) * HD;
+      uint8_t* dq = sQ + qbuf * C::QB;
+#pragma unroll
+      for (int ch = 0; ch < HD / 8; ++ch)
+        cp_async16(dq + (ch >> 3) * ROWS * 128 + tl * 128 + (((ch & 7) ^ (tl & 7)) << 4), src + ch * 8, lv);
+      cp_commit();
+    };
+    auto q_ready = [&](int qbuf) {
+      cp_wait_all();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_full[qbuf]);
+    };
+    if (set == 0 && n_mine > 0) {
+      load_q(cur, 0);
+      q_ready(0);
+    }
+#endif
     for (int k = 0; k < n_mine; ++k, ++items) {
       Item nn;   // the item after next: its fields load while this item runs
       if (k + 2 < n_mine) nn = item_info(k + 2);
+#ifdef HM_TC_QCPASYNC
+      bool q_pending = false;
+      if (set == 0 && k + 1 < n_mine) {   // item k + 1's tile: buffer free once item k - 1's S are done
+        if (k >= 1) MBAR_WAIT(&q_empty[(k + 1) & 1], ((k - 1) >> 1) & 1, 15, k);
+        load_q(nxt, (k + 1) & 1);
+        q_pending = true;
+      }
+#endif
       if (quarter == 2 && lane == 0) TC_TRACE(set == 0 ? 8 : 12, items);
       const int rows_here = tile_rows(cur.qlen, cur.tile), n_stage = cur.n_stage;
       int hpos[2][2];   // position of row (half, a/b); -1: padding row, fully masked
@@ -623,7 +669,16 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b]);
         if (quarter == 2 && lane == 0) TC_TRACE(3, gs);
+#ifdef HM_TC_QCPASYNC
+        if (q_pending) {
+          q_ready((k + 1) & 1);
+          q_pending = false;
+        }
+#endif
       }
+#ifdef HM_TC_QCPASYNC
+      if (q_pending) q_ready((k + 1) & 1);
+#endif
       if (quarter == 2 && lane == 0) TC_TRACE(set == 0 ? 10 : 13, items);
       // gather each row's sum of P (the 4 threads of a row, both sets) into l_sh
 #pragma unroll
