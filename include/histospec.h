@@ -24,6 +24,9 @@
  *          (replay: truth supplied; greedy: truth = argmax of the verify rows)
  *   hs_replay_fused
  *       -> spec_engine.py:260-279 replay_response, whole responses per launch
+ *   hs_similarity_replay
+ *       -> tracegen.py:306-353 token_similarity_replay (the paper's 5.1
+ *          prefix-search similarity metric), one warp per response
  */
 #ifndef HISTOSPEC_H_
 #define HISTOSPEC_H_
@@ -160,6 +163,14 @@ int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int32_t* d_slo
                     const int32_t* d_truth, const int64_t* d_truth_off, const uint8_t* d_speculate,
                     int32_t* d_tpi, int32_t* d_n_iter, int64_t* d_stats, HsSpecConfig cfg,
                     hs_stream_t stream);
+
+/* Token-similarity replay over an index of the previous epoch's responses:
+ * response r (tokens d_tokens[d_resp_off[r] : d_resp_off[r+1]]) is replayed
+ * against slot d_slot_of_resp[r]; d_accepted[r] = tokens accepted by the
+ * prefix search (tracegen.py:306-353).  prefix_len < 1 -> HS_ERR_INVALID. */
+int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, const int32_t* d_tokens,
+                         const int64_t* d_resp_off, const int32_t* d_slot_of_resp, int32_t prefix_len,
+                         int64_t* d_accepted, hs_stream_t stream);
 
 #ifdef __cplusplus
 }

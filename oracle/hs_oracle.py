@@ -187,3 +187,40 @@ def replay(truth, corpus, cfg: Config, speculate=True, draft_fn=None):
         out.accepted += appended
     assert gen == list(truth)
     return out
+
+
+def token_similarity_replay(prev, cur, prefix_len):
+    """(accepted, total, warmup) of the prefix-search replay (TEST INFRASTRUCTURE ONLY).
+
+    Restates `rhymesim/tracegen.py:306-353` on plain dicts
+    `{prompt_id: [token list, ...]}` for the two epochs.  Only prompts present
+    in both epochs count (`:328`).  At each position the longest identical
+    continuation over every occurrence of the last `prefix_len` tokens in the
+    prompt's previous-epoch responses is found by a direct scan of all
+    history positions (no n-gram dict), stopping at either response's end.
+    """
+    if prefix_len < 1:
+        raise ValueError("prefix_len must be >= 1")
+    accepted = total = warmup = 0
+    for pid in sorted(set(prev) & set(cur)):
+        history = [list(h) for h in prev[pid]]
+        for tokens in cur[pid]:
+            tokens = list(tokens)
+            n = len(tokens)
+            total += n
+            warmup += min(prefix_len, n)
+            pos = prefix_len
+            while pos < n:
+                key = tokens[pos - prefix_len:pos]
+                best = 0
+                for hist in history:
+                    for end in range(prefix_len, len(hist) + 1):
+                        if hist[end - prefix_len:end] != key:
+                            continue
+                        run = 0
+                        while pos + run < n and end + run < len(hist) and hist[end + run] == tokens[pos + run]:
+                            run += 1
+                        best = max(best, run)
+                pos += best if best > 0 else 1
+                accepted += best
+    return accepted, total, warmup

@@ -61,6 +61,7 @@ SIGNATURES = {
     "hs_accept_greedy": [_I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _I32, _P,
                          HsSpecConfig, _P],
     "hs_replay_fused": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _P, _P, _P, _P, _P, HsSpecConfig, _P],
+    "hs_similarity_replay": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _P, _I32, _P, _P],
 }
 
 _lib = None

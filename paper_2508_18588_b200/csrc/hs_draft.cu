@@ -508,6 +508,70 @@ __global__ void __launch_bounds__(256, 8) k_draft4(HsIndexView V, int32_t n_seq,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Token-similarity replay (tracegen.py:306-353 token_similarity_replay).
+//
+// The reference indexes every prefix_len-gram of the previous epoch's
+// responses and, at each position, scans all occurrences of the last p
+// tokens for the longest identical continuation.  That maximum equals
+// (longest prefix of Q = tokens[pos-p : len] occurring in the prompt's
+// history) - p, when that prefix reaches length p.  The suffix with the
+// longest common prefix with Q is adjacent to Q's insertion point in the
+// slot's suffix array, so one warp binary search per step replaces the scan.
+// The terminal (-1) ends every history response and sorts below all tokens;
+// the end of Q sorts below the terminal.
+
+// LCP of suffix text[p:] with q[0:qn] and the three-way order (suffix vs q).
+__device__ __forceinline__ int32_t lcp_query(const int32_t* __restrict__ text, int32_t p,
+                                             const int32_t* __restrict__ q, int32_t qn, int* order) {
+  const int lane = lane_id();
+  for (int32_t c = 0;; c += 32) {
+    int32_t j = c + lane;
+    int32_t a = text[p + j];      // in bounds: a terminal lies within 32 tokens ahead or HS_TEXT_PAD covers it
+    int32_t b = j < qn ? q[j] : -2;
+    unsigned d = __ballot_sync(0xffffffffu, a != b || a < 0);
+    if (d) {
+      int src = __ffs(d) - 1;
+      int32_t x = __shfl_sync(0xffffffffu, a, src);
+      int32_t y = __shfl_sync(0xffffffffu, b, src);
+      *order = x < y ? -1 : 1;    // x == y only when both are terminals' stand-ins: never (-1 vs -2)
+      return c + src;
+    }
+  }
+}
+
+__global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t* __restrict__ tok,
+                                    const int64_t* __restrict__ off, const int32_t* __restrict__ slot_of,
+                                    int32_t p, int64_t* __restrict__ accepted) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_resp) return;
+  const int32_t* t = tok + off[r];
+  const int32_t len = (int32_t)(off[r + 1] - off[r]);
+  const int32_t slot = slot_of[r];
+  const int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
+  int64_t acc = 0;
+  if (S < E) {
+    for (int32_t pos = p; pos < len;) {
+      const int32_t* q = t + pos - p;
+      const int32_t qn = len - pos + p;
+      int64_t lo = S, hi = E;
+      int32_t l_lo = 0, l_hi = 0;   // LCP with the last suffix found below / above q
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        int order;
+        int32_t l = lcp_query(V.text, V.sa[mid], q, qn, &order);
+        if (order < 0) { lo = mid + 1; l_lo = l; } else { hi = mid; l_hi = l; }
+      }
+      // the last probes on either side are the insertion point's neighbours sa[lo - 1] and sa[lo]
+      // (lo only moves to mid + 1, hi only to mid); a side never probed has no neighbour
+      const int32_t best = max(l_lo, l_hi);
+      int32_t run = best - p;
+      if (run > 0) { acc += run; pos += run; } else { pos += 1; }
+    }
+  }
+  if (lane_id() == 0) accepted[r] = acc;
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -574,6 +638,20 @@ extern "C" int hs_draft(const HsIndexView* view, int32_t n_seq, const int32_t* d
                                                                  d_gen_len, d_prefix_len, d_window, d_speculate,
                                                                  d_draft_tok, draft_stride, d_draft_len, d_looked,
                                                                  d_found);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
+extern "C" int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, const int32_t* d_tokens,
+                                    const int64_t* d_resp_off, const int32_t* d_slot_of_resp, int32_t prefix_len,
+                                    int64_t* d_accepted, hs_stream_t stream) {
+  if (prefix_len < 1) { hs_set_error("prefix_len must be >= 1"); return HS_ERR_INVALID; }
+  if (n_resp <= 0) return HS_OK;
+  const int threads = 256;
+  const int64_t blocks = ((int64_t)n_resp * 32 + threads - 1) / threads;
+  hs_count_launches(1);
+  k_similarity_replay<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n_resp, d_tokens, d_resp_off,
+                                                                            d_slot_of_resp, prefix_len, d_accepted);
   HS_CUDA_TRY(cudaGetLastError());
   return HS_OK;
 }
