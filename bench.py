@@ -2,7 +2,7 @@
 """HistoSpec B200 benchmark (driver contract: one JSON line on rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload rollout|replay|lookup]
+                  [--workload rollout|replay|lookup|similarity]
 
 Workloads (all on BASELINE.json configs[1] shapes, synthetic, seeded):
   rollout  greedy HistoSpec rollout of the Qwen2.5-1.5B-shaped random-init
@@ -602,6 +602,54 @@ def run_lookup(args, dist, pk):
     }, data
 
 
+def run_similarity(args, dist, pk):
+    """token_similarity_replay (tracegen.py:306-353) of a configs[1]-sized epoch pair: every
+    truth response replayed against its prompt's (D) history in one hs_similarity_replay launch."""
+    import torch
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.similarity import replay_against_index
+
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    wl, data = replay_setup(args, dist.rank)
+    idx = GpuIndex.from_arrays(torch.from_numpy(data["hist_tokens"]).to(dev), data["resp_off"],
+                               data["slot_resp_off"], data["reward_fx"])
+    truths = data["truths"]
+    n, L = truths.shape
+    d_tok = torch.from_numpy(truths.reshape(-1).astype(np.int32)).to(dev)
+    d_off = torch.arange(0, (n + 1) * L, L, dtype=torch.int64, device=dev)
+    d_slot = torch.from_numpy(data["truth_slots"]).to(dev)
+    plen = 3
+    stream = torch.cuda.current_stream(dev)
+    out = [None]
+
+    def launch():
+        out[0] = replay_against_index(idx, d_tok, d_off, d_slot, plen, stream=stream)
+
+    ms, clocks = timed(launch, args.steps, args.warmup, dist, stream, dist.local)
+    acc = int(out[0].sum().item())
+    tokens = n * L
+    # lower bound on search steps: every non-accepted position after the warm-up is one search
+    steps = tokens - n * plen - acc
+    depth = int(np.ceil(np.log2(max(2, idx.n_tokens // max(1, idx.n_slots)))))
+    alg = 4 * tokens + steps * depth * 8
+    achieved = alg / (ms / 1e3) / 1e9
+    return {
+        "metric": "similarity-replay tokens/sec (token_similarity_replay, prefix_len 3)",
+        "value": dist.sum(tokens) / (ms / 1e3), "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{n} responses x {L} tokens vs {args.prompts} prompts x 8 (D) histories "
+                               f"(s = {args.similarity})", "l2": "index + responses exceed L2"},
+        "acceptance": acc / tokens, "acceptance_after_warmup": acc / max(1, tokens - n * plen),
+        "roofline": {"kernel": "k_similarity_replay", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                     "note": "latency-bound dependent binary searches; bytes = 4/token + 8 per search probe "
+                             "(lower bound on probes)"},
+        "gpu_launches": 1, "clocks": clocks,
+    }, data
+
+
 # ------------------------------------------------------------------ reference arm
 
 def run_reference(args, dist):
@@ -643,7 +691,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup"])
+    ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup", "similarity"])
     ap.add_argument("--model", default="qwen2.5-1.5b-shape")
     ap.add_argument("--batch", type=int, default=1024, help="resident sequences per wave (rollout)")
     ap.add_argument("--prompt-len", type=int, default=256)
@@ -678,6 +726,8 @@ def main():
         line, data = run_rollout(args, dist, pk)
     elif args.workload == "replay":
         line, data = run_replay(args, dist, pk)
+    elif args.workload == "similarity":
+        line, data = run_similarity(args, dist, pk)
     else:
         line, data = run_lookup(args, dist, pk)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
