@@ -602,6 +602,23 @@ def run_lookup(args, dist, pk):
     }, data
 
 
+def cpu_similarity_sample(data, prompts, prefix_len):
+    """The reference's algorithm (oracle restatement with its dict-of-grams index, tracegen.py:306-353)
+    on one host core over the first `prompts` prompts of the same epoch pair."""
+    from oracle import hs_oracle
+    from paper_2508_18588_b200.workload import history_lists
+    hl = history_lists(data)
+    samples = data["truths"].shape[0] // len(hl)
+    prev = {p: [t.tolist() for t, _ in hl[p]] for p in range(prompts)}
+    cur = {p: [data["truths"][p * samples + i].tolist() for i in range(samples)] for p in range(prompts)}
+    t0 = time.perf_counter()
+    acc, total, _ = hs_oracle.token_similarity_replay_indexed(prev, cur, prefix_len)
+    dt = time.perf_counter() - t0
+    return {"value": total / dt, "accepted": acc,
+            "sample": f"{prompts} prompts x {samples} responses (first prompts of the same epoch pair), "
+                      f"dict-of-grams replay, 1 thread"}
+
+
 def run_similarity(args, dist, pk):
     """token_similarity_replay (tracegen.py:306-353) of a configs[1]-sized epoch pair: every
     truth response replayed against its prompt's (D) history in one hs_similarity_replay launch."""
@@ -735,6 +752,10 @@ def main():
         if args.workload == "replay":
             r = cpu_replay_sample(data, args.ref_prompts, threads)
             line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": threads, "kind": "port",
+                                    "sample": r["sample"]}
+        elif args.workload == "similarity":
+            r = cpu_similarity_sample(data, min(64, args.prompts), 3)
+            line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": 1, "kind": "port",
                                     "sample": r["sample"]}
         elif args.workload == "rollout":
             r, _ = cpu_rollout_sample(data["cfg"], args.seed, data["prompts"][:args.cpu_seqs * args.samples:

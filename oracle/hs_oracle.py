@@ -224,3 +224,38 @@ def token_similarity_replay(prev, cur, prefix_len):
                 pos += best if best > 0 else 1
                 accepted += best
     return accepted, total, warmup
+
+
+def token_similarity_replay_indexed(prev, cur, prefix_len):
+    """Same result as `token_similarity_replay`, with the reference's own data structure: a dict
+    from each prefix_len-gram of the history to its (response, end) occurrences
+    (`tracegen.py:329-334`), scanned per step (`:341-352`).  This is the reference's CPU cost
+    model; bench.py times it (single core) as the similarity workload's cpu_baseline."""
+    if prefix_len < 1:
+        raise ValueError("prefix_len must be >= 1")
+    accepted = total = warmup = 0
+    for pid in sorted(set(prev) & set(cur)):
+        history = [list(h) for h in prev[pid]]
+        grams = {}
+        for hi, hist in enumerate(history):
+            for end in range(prefix_len, len(hist) + 1):
+                grams.setdefault(tuple(hist[end - prefix_len:end]), []).append((hi, end))
+        for tokens in cur[pid]:
+            tokens = list(tokens)
+            n = len(tokens)
+            total += n
+            warmup += min(prefix_len, n)
+            pos = prefix_len
+            while pos < n:
+                best = 0
+                for hi, end in grams.get(tuple(tokens[pos - prefix_len:pos]), ()):
+                    hist = history[hi]
+                    lim = min(n - pos, len(hist) - end)
+                    run = 0
+                    while run < lim and hist[end + run] == tokens[pos + run]:
+                        run += 1
+                    if run > best:
+                        best = run
+                pos += best if best > 0 else 1
+                accepted += best
+    return accepted, total, warmup

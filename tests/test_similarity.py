@@ -23,8 +23,11 @@ def test_oracle_matches_reference_golden():
         tr = _epochs(case)
         for r in case["results"]:
             a, b = r["pair"]
+            want = (r["accepted"], r["total"], r["warmup"])
             got = hs_oracle.token_similarity_replay(tr.get(a, {}), tr.get(b, {}), r["prefix_len"])
-            assert got == (r["accepted"], r["total"], r["warmup"]), (r, got)
+            assert got == want, (r, got)
+            got = hs_oracle.token_similarity_replay_indexed(tr.get(a, {}), tr.get(b, {}), r["prefix_len"])
+            assert got == want, (r, got)
 
 
 def test_oracle_rejects_bad_prefix():
