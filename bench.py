@@ -649,7 +649,9 @@ def run_similarity(args, dist, pk):
     # lower bound on search steps: every non-accepted position after the warm-up is one search
     steps = tokens - n * plen - acc
     depth = int(np.ceil(np.log2(max(2, idx.n_tokens // max(1, idx.n_slots)))))
-    alg = 4 * tokens + steps * depth * 8
+    # response read once + the matched history continuation read once + an SA entry and a text chunk head
+    # per probe
+    alg = 4 * tokens + 4 * acc + steps * depth * 8
     achieved = alg / (ms / 1e3) / 1e9
     return {
         "metric": "similarity-replay tokens/sec (token_similarity_replay, prefix_len 3)",
@@ -661,8 +663,8 @@ def run_similarity(args, dist, pk):
         "acceptance": acc / tokens, "acceptance_after_warmup": acc / max(1, tokens - n * plen),
         "roofline": {"kernel": "k_similarity_replay", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                     "note": "latency-bound dependent binary searches; bytes = 4/token + 8 per search probe "
-                             "(lower bound on probes)"},
+                     "note": "latency-bound dependent binary searches; bytes = 4 per response token + 4 per "
+                             "accepted token + 8 per search probe (lower bound on probes)"},
         "gpu_launches": 1, "clocks": clocks,
     }, data
 

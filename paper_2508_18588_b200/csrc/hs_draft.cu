@@ -11,6 +11,7 @@
 // then the locus node from a warp min-scan of the LCP values inside the
 // interval.
 #include <cstdlib>
+#include <string>
 
 #include "hs_common.cuh"
 
@@ -521,34 +522,48 @@ __global__ void __launch_bounds__(256, 8) k_draft4(HsIndexView V, int32_t n_seq,
 // The terminal (-1) ends every history response and sorts below all tokens;
 // the end of Q sorts below the terminal.
 
-// LCP of suffix text[p:] with q[0:qn] and the three-way order (suffix vs q).
-__device__ __forceinline__ int32_t lcp_query(const int32_t* __restrict__ text, int32_t p,
-                                             const int32_t* __restrict__ q, int32_t qn, int* order) {
+// LCP of suffix text[p:] with q[0:qn] and the three-way order (suffix vs q); the first k0
+// tokens are known to be equal.  Four 32-token chunks are loaded per round so a long match
+// costs a quarter of the dependent round trips; text reads are clamped to the padded text.
+template <int U>
+__device__ __forceinline__ int32_t lcp_query(const int32_t* __restrict__ text, int64_t text_end, int32_t p,
+                                             const int32_t* __restrict__ q, int32_t qn, int32_t k0, int* order) {
   const int lane = lane_id();
-  for (int32_t c = 0;; c += 32) {
-    int32_t j = c + lane;
-    int32_t a = text[p + j];      // in bounds: a terminal lies within 32 tokens ahead or HS_TEXT_PAD covers it
-    int32_t b = j < qn ? q[j] : -2;
-    unsigned d = __ballot_sync(0xffffffffu, a != b || a < 0);
-    if (d) {
-      int src = __ffs(d) - 1;
-      int32_t x = __shfl_sync(0xffffffffu, a, src);
-      int32_t y = __shfl_sync(0xffffffffu, b, src);
-      *order = x < y ? -1 : 1;    // x == y only when both are terminals' stand-ins: never (-1 vs -2)
-      return c + src;
+  for (int32_t c = k0;; c += 32 * U) {
+    int32_t a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t j = c + 32 * u + lane;
+      a[u] = text[min((int64_t)p + j, text_end)];
+      b[u] = j < qn ? q[j] : -2;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      // the first flagged lane lies at or before the suffix's terminal, so clamped reads never decide
+      unsigned d = __ballot_sync(0xffffffffu, a[u] != b[u] || a[u] < 0);
+      if (d) {
+        int src = __ffs(d) - 1;
+        int32_t x = __shfl_sync(0xffffffffu, a[u], src);
+        int32_t y = __shfl_sync(0xffffffffu, b[u], src);
+        *order = x < y ? -1 : 1;    // never equal: a terminal (-1) meets q's end only as -2
+        return c + 32 * u + src;
+      }
     }
   }
 }
 
+template <int U, bool PREFETCH>
 __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t* __restrict__ tok,
                                     const int64_t* __restrict__ off, const int32_t* __restrict__ slot_of,
                                     int32_t p, int64_t* __restrict__ accepted) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= n_resp) return;
+  const int lane = lane_id();
   const int32_t* t = tok + off[r];
   const int32_t len = (int32_t)(off[r + 1] - off[r]);
   const int32_t slot = slot_of[r];
   const int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
+  const int64_t text_end = V.n_text + HS_TEXT_PAD - 1;
   int64_t acc = 0;
   if (S < E) {
     for (int32_t pos = p; pos < len;) {
@@ -556,11 +571,24 @@ __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t
       const int32_t qn = len - pos + p;
       int64_t lo = S, hi = E;
       int32_t l_lo = 0, l_hi = 0;   // LCP with the last suffix found below / above q
+      int64_t mid = (lo + hi) >> 1;
+      int32_t sp = V.sa[mid];
       while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
+        // prefetch both possible next probes (lane 0: left half, lane 1: right half) so the SA
+        // load leaves the dependent chain; one text round trip per probe remains
+        const int64_t mid_l = (lo + mid) >> 1, mid_r = (mid + 1 + hi) >> 1;
+        const int64_t nxt = lane == 0 ? mid_l : mid_r;
+        const int32_t sp_n = (PREFETCH && lane < 2 && nxt < E) ? V.sa[nxt] : 0;
         int order;
-        int32_t l = lcp_query(V.text, V.sa[mid], q, qn, &order);
-        if (order < 0) { lo = mid + 1; l_lo = l; } else { hi = mid; l_hi = l; }
+        // every suffix between the two bracketing probes shares min(l_lo, l_hi) tokens with q
+        int32_t l = lcp_query<U>(V.text, text_end, sp, q, qn, min(l_lo, l_hi), &order);
+        int32_t sp_l = __shfl_sync(0xffffffffu, sp_n, 0), sp_r = __shfl_sync(0xffffffffu, sp_n, 1);
+        if (!PREFETCH) {
+          const int64_t m2 = order < 0 ? mid_r : mid_l;   // only the taken side, after the compare
+          sp_l = sp_r = m2 < E ? V.sa[m2] : 0;
+        }
+        if (order < 0) { lo = mid + 1; l_lo = l; mid = mid_r; sp = sp_r; }
+        else { hi = mid; l_hi = l; mid = mid_l; sp = sp_l; }
       }
       // the last probes on either side are the insertion point's neighbours sa[lo - 1] and sa[lo]
       // (lo only moves to mid + 1, hi only to mid); a side never probed has no neighbour
@@ -569,7 +597,7 @@ __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t
       if (run > 0) { acc += run; pos += run; } else { pos += 1; }
     }
   }
-  if (lane_id() == 0) accepted[r] = acc;
+  if (lane == 0) accepted[r] = acc;
 }
 
 }  // namespace hs
@@ -649,9 +677,16 @@ extern "C" int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, con
   if (n_resp <= 0) return HS_OK;
   const int threads = 256;
   const int64_t blocks = ((int64_t)n_resp * 32 + threads - 1) / threads;
+  // A/B switch for profiling only: HS_SIM_VARIANT = u1 (default) | u2 | u4 | u1np (no SA prefetch)
+  static const char* var_env = getenv("HS_SIM_VARIANT");
+  const std::string var = var_env ? var_env : "u1";
+  auto kern = k_similarity_replay<1, true>;
+  if (var == "u2") kern = k_similarity_replay<2, true>;
+  else if (var == "u4") kern = k_similarity_replay<4, true>;
+  else if (var == "u1np") kern = k_similarity_replay<1, false>;
   hs_count_launches(1);
-  k_similarity_replay<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n_resp, d_tokens, d_resp_off,
-                                                                            d_slot_of_resp, prefix_len, d_accepted);
+  kern<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n_resp, d_tokens, d_resp_off, d_slot_of_resp,
+                                                               prefix_len, d_accepted);
   HS_CUDA_TRY(cudaGetLastError());
   return HS_OK;
 }
