@@ -552,7 +552,13 @@ __device__ __forceinline__ int32_t lcp_query(const int32_t* __restrict__ text, i
   }
 }
 
-template <int U, bool PREFETCH>
+// LCP-array bound (LCPB): when one bracket shares more with q than the other, the LCP array
+// decides a probe without touching the text whenever the range to that bracket is short:
+// x = LCP(bracket, probe) = min lcp[] over the range; x > l -> same side as the bracket with LCP l,
+// x < l -> the other side with LCP x, x == l -> compare from l.
+constexpr int64_t kSimLcpScan = 256;
+
+template <int U, bool PREFETCH, bool LCPB = false>
 __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t* __restrict__ tok,
                                     const int64_t* __restrict__ off, const int32_t* __restrict__ slot_of,
                                     int32_t p, int64_t* __restrict__ accepted) {
@@ -579,9 +585,23 @@ __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t
         const int64_t mid_l = (lo + mid) >> 1, mid_r = (mid + 1 + hi) >> 1;
         const int64_t nxt = lane == 0 ? mid_l : mid_r;
         const int32_t sp_n = (PREFETCH && lane < 2 && nxt < E) ? V.sa[nxt] : 0;
-        int order;
+        int order = 0;
         // every suffix between the two bracketing probes shares min(l_lo, l_hi) tokens with q
-        int32_t l = lcp_query<U>(V.text, text_end, sp, q, qn, min(l_lo, l_hi), &order);
+        int32_t k0 = min(l_lo, l_hi), l = -1;
+        if (LCPB && l_lo != l_hi) {
+          const bool low = l_lo > l_hi;
+          const int64_t a = low ? lo : mid + 1, b = low ? mid : hi;   // lcp[a..b] spans bracket..probe
+          if ((low ? lo > S : hi < E) && b - a < kSimLcpScan) {
+            int32_t x = 0x7fffffff;
+            for (int64_t k = a + lane; k <= b; k += 32) x = min(x, V.lcp[k]);
+            x = __reduce_min_sync(0xffffffffu, x);
+            const int32_t lb = low ? l_lo : l_hi;
+            if (x > lb) { order = low ? -1 : 1; l = lb; }
+            else if (x < lb) { order = low ? 1 : -1; l = x; }
+            else k0 = lb;
+          }
+        }
+        if (l < 0) l = lcp_query<U>(V.text, text_end, sp, q, qn, k0, &order);
         int32_t sp_l = __shfl_sync(0xffffffffu, sp_n, 0), sp_r = __shfl_sync(0xffffffffu, sp_n, 1);
         if (!PREFETCH) {
           const int64_t m2 = order < 0 ? mid_r : mid_l;   // only the taken side, after the compare
@@ -677,13 +697,14 @@ extern "C" int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, con
   if (n_resp <= 0) return HS_OK;
   const int threads = 256;
   const int64_t blocks = ((int64_t)n_resp * 32 + threads - 1) / threads;
-  // A/B switch for profiling only: HS_SIM_VARIANT = u1 (default) | u2 | u4 | u1np (no SA prefetch)
+  // A/B switch for profiling only: HS_SIM_VARIANT = u1 (default) | u2 | u4 | u1np (no SA prefetch) | lcp (LCP-array bound)
   static const char* var_env = getenv("HS_SIM_VARIANT");
   const std::string var = var_env ? var_env : "u1";
   auto kern = k_similarity_replay<1, true>;
   if (var == "u2") kern = k_similarity_replay<2, true>;
   else if (var == "u4") kern = k_similarity_replay<4, true>;
   else if (var == "u1np") kern = k_similarity_replay<1, false>;
+  else if (var == "lcp") kern = k_similarity_replay<1, true, true>;
   hs_count_launches(1);
   kern<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n_resp, d_tokens, d_resp_off, d_slot_of_resp,
                                                                prefix_len, d_accepted);
