@@ -24,7 +24,7 @@
  *          (replay: truth supplied; greedy: truth = argmax of the verify rows)
  *   hs_replay_fused
  *       -> spec_engine.py:260-279 replay_response, whole responses per launch
- *   hs_similarity_replay
+ *   hs_similarity_replay / hs_similarity_replay_isa (+ hs_index_inverse_sa)
  *       -> tracegen.py:306-353 token_similarity_replay (the paper's 5.1
  *          prefix-search similarity metric), one warp per response
  */
@@ -171,6 +171,15 @@ int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int32_t* d_slo
 int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, const int32_t* d_tokens,
                          const int64_t* d_resp_off, const int32_t* d_slot_of_resp, int32_t prefix_len,
                          int64_t* d_accepted, hs_stream_t stream);
+
+/* Inverse suffix array of an index: d_isa[n_text] (int32), d_isa[sa[k]] = k, -1 at terminals. */
+int hs_index_inverse_sa(const HsIndexView* view, int32_t* d_isa, hs_stream_t stream);
+
+/* hs_similarity_replay seeded by the inverse suffix array (same results): each search after an
+ * accepted run starts from the rank of the matched suffix advanced by the run. */
+int hs_similarity_replay_isa(const HsIndexView* view, const int32_t* d_isa, int32_t n_resp,
+                             const int32_t* d_tokens, const int64_t* d_resp_off, const int32_t* d_slot_of_resp,
+                             int32_t prefix_len, int64_t* d_accepted, hs_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,8 @@ SIGNATURES = {
                          HsSpecConfig, _P],
     "hs_replay_fused": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _P, _P, _P, _P, _P, HsSpecConfig, _P],
     "hs_similarity_replay": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _P, _I32, _P, _P],
+    "hs_index_inverse_sa": [ctypes.POINTER(HsIndexView), _P, _P],
+    "hs_similarity_replay_isa": [ctypes.POINTER(HsIndexView), _P, _I32, _P, _P, _P, _I32, _P, _P],
 }
 
 _lib = None

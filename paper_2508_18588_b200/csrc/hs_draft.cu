@@ -620,6 +620,84 @@ __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t
   if (lane == 0) accepted[r] = acc;
 }
 
+
+// Inverse suffix array: isa[sa[k]] = k (terminal positions stay -1).
+__global__ void k_inverse_sa(const int32_t* __restrict__ sa, int64_t n_suffix, int32_t* __restrict__ isa) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_suffix; k += (int64_t)gridDim.x * blockDim.x)
+    isa[sa[k]] = (int32_t)k;
+}
+
+// ISA-seeded variant: after a run of `run` tokens matched by suffix h, suffix h + run shares the
+// next query's first p tokens, so its rank (isa) seeds the next search.  A gallop from that rank
+// brackets the insertion point within the p-gram's SA interval; a binary search finishes it.
+// Misses (run 0) fall back to a full search.
+__global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict__ isa, int32_t n_resp,
+                                        const int32_t* __restrict__ tok, const int64_t* __restrict__ off,
+                                        const int32_t* __restrict__ slot_of, int32_t p,
+                                        int64_t* __restrict__ accepted) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_resp) return;
+  const int lane = lane_id();
+  const int32_t* t = tok + off[r];
+  const int32_t len = (int32_t)(off[r + 1] - off[r]);
+  const int32_t slot = slot_of[r];
+  const int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
+  const int64_t text_end = V.n_text + HS_TEXT_PAD - 1;
+  int64_t acc = 0;
+  if (S < E) {
+    int64_t hint = -1;   // SA index of a suffix sharing >= p tokens with the query, or -1
+    for (int32_t pos = p; pos < len;) {
+      const int32_t* q = t + pos - p;
+      const int32_t qn = len - pos + p;
+      int64_t lo = S, hi = E;
+      int32_t l_lo = 0, l_hi = 0, sp_lo = -1, sp_hi = -1;   // bracketing probes: LCP and text position
+      int order;
+      if (hint >= 0) {
+        const int32_t sp0 = V.sa[hint];
+        const int32_t l0 = lcp_query<1>(V.text, text_end, sp0, q, qn, p, &order);
+        if (order < 0) {
+          lo = hint + 1; l_lo = l0; sp_lo = sp0;
+          for (int64_t step = 1;; step <<= 1) {
+            const int64_t k = hint + step;
+            if (k >= E) break;
+            const int32_t sp = V.sa[k];
+            const int32_t l = lcp_query<1>(V.text, text_end, sp, q, qn, 0, &order);
+            if (order < 0) { lo = k + 1; l_lo = l; sp_lo = sp; }
+            else { hi = k; l_hi = l; sp_hi = sp; break; }
+          }
+        } else {
+          hi = hint; l_hi = l0; sp_hi = sp0;
+          for (int64_t step = 1;; step <<= 1) {
+            const int64_t k = hint - step;
+            if (k < S) break;
+            const int32_t sp = V.sa[k];
+            const int32_t l = lcp_query<1>(V.text, text_end, sp, q, qn, 0, &order);
+            if (order < 0) { lo = k + 1; l_lo = l; sp_lo = sp; break; }
+            else { hi = k; l_hi = l; sp_hi = sp; }
+          }
+        }
+      }
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int32_t sp = V.sa[mid];
+        const int32_t l = lcp_query<1>(V.text, text_end, sp, q, qn, min(l_lo, l_hi), &order);
+        if (order < 0) { lo = mid + 1; l_lo = l; sp_lo = sp; } else { hi = mid; l_hi = l; sp_hi = sp; }
+      }
+      const int32_t best = max(l_lo, l_hi);
+      const int32_t run = best - p;
+      if (run > 0) {
+        acc += run;
+        pos += run;
+        hint = isa[(l_lo >= l_hi ? sp_lo : sp_hi) + run];
+      } else {
+        pos += 1;
+        hint = -1;
+      }
+    }
+  }
+  if (lane == 0) accepted[r] = acc;
+}
+
 }  // namespace hs
 
 using namespace hs;
@@ -708,6 +786,31 @@ extern "C" int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, con
   hs_count_launches(1);
   kern<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n_resp, d_tokens, d_resp_off, d_slot_of_resp,
                                                                prefix_len, d_accepted);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
+extern "C" int hs_index_inverse_sa(const HsIndexView* view, int32_t* d_isa, hs_stream_t stream) {
+  HS_CUDA_TRY(cudaMemsetAsync(d_isa, 0xff, sizeof(int32_t) * (size_t)(view->n_text > 0 ? view->n_text : 1),
+                              (cudaStream_t)stream));
+  if (view->n_suffix <= 0) return HS_OK;
+  hs_count_launches(1);
+  k_inverse_sa<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(view->sa, view->n_suffix, d_isa);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
+extern "C" int hs_similarity_replay_isa(const HsIndexView* view, const int32_t* d_isa, int32_t n_resp,
+                                        const int32_t* d_tokens, const int64_t* d_resp_off,
+                                        const int32_t* d_slot_of_resp, int32_t prefix_len, int64_t* d_accepted,
+                                        hs_stream_t stream) {
+  if (prefix_len < 1) { hs_set_error("prefix_len must be >= 1"); return HS_ERR_INVALID; }
+  if (n_resp <= 0) return HS_OK;
+  const int threads = 256;
+  const int64_t blocks = ((int64_t)n_resp * 32 + threads - 1) / threads;
+  hs_count_launches(1);
+  k_similarity_replay_isa<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      *view, d_isa, n_resp, d_tokens, d_resp_off, d_slot_of_resp, prefix_len, d_accepted);
   HS_CUDA_TRY(cudaGetLastError());
   return HS_OK;
 }

@@ -13,12 +13,18 @@ There is no CPU fallback: without CUDA the call raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
 from .index import GpuIndex
+
+
+# "isa": ISA-seeded searches (hs_similarity_replay_isa); anything else: plain searches
+# (hs_similarity_replay, whose kernel family HS_SIM_VARIANT also selects in the library)
+_VARIANT = os.environ.get("HS_SIM_VARIANT", "u1")
 
 
 @dataclass(frozen=True)
@@ -64,10 +70,21 @@ def replay_against_index(index: GpuIndex, d_tokens, resp_off, slot_of_resp, pref
     dev = d_tokens.device
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     out = torch.zeros(n, dtype=torch.int64, device=dev)
+    lib = _lib.load()
     with torch.cuda.device(dev):
-        _lib.check(_lib.load().hs_similarity_replay(
-            ctypes.byref(index.view), n, d_tokens.data_ptr(), resp_off.data_ptr(), slot_of_resp.data_ptr(),
-            int(prefix_len), out.data_ptr(), s.cuda_stream))
+        if _VARIANT == "isa":
+            isa = getattr(index, "_isa", None)
+            if isa is None:
+                isa = torch.empty(max(1, index.view.n_text), dtype=torch.int32, device=dev)
+                _lib.check(lib.hs_index_inverse_sa(ctypes.byref(index.view), isa.data_ptr(), s.cuda_stream))
+                index._isa = isa      # 4 B per indexed token, kept with the index
+            _lib.check(lib.hs_similarity_replay_isa(
+                ctypes.byref(index.view), isa.data_ptr(), n, d_tokens.data_ptr(), resp_off.data_ptr(),
+                slot_of_resp.data_ptr(), int(prefix_len), out.data_ptr(), s.cuda_stream))
+        else:
+            _lib.check(lib.hs_similarity_replay(
+                ctypes.byref(index.view), n, d_tokens.data_ptr(), resp_off.data_ptr(), slot_of_resp.data_ptr(),
+                int(prefix_len), out.data_ptr(), s.cuda_stream))
     return out
 
 
