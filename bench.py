@@ -661,7 +661,7 @@ def run_similarity(args, dist, pk):
         "config": {"workload": f"{n} responses x {L} tokens vs {args.prompts} prompts x 8 (D) histories "
                                f"(s = {args.similarity})", "l2": "index + responses exceed L2"},
         "acceptance": acc / tokens, "acceptance_after_warmup": acc / max(1, tokens - n * plen),
-        "roofline": {"kernel": "k_similarity_replay", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
+        "roofline": {"kernel": "k_similarity_replay_isa", "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
                      "note": "latency-bound dependent binary searches; bytes = 4 per response token + 4 per "
                              "accepted token + 8 per search probe (lower bound on probes)"},

@@ -47,8 +47,16 @@ def _to_trace(tr):
     return {e: {pid: [(t, 0.0) for t in rs] for pid, rs in d.items()} for e, d in tr.items()}
 
 
+@pytest.fixture(params=["isa", "u1"])
+def variant(request, monkeypatch):
+    """Both search kernels: ISA-seeded (default) and plain binary search."""
+    from paper_2508_18588_b200 import similarity
+    monkeypatch.setattr(similarity, "_VARIANT", request.param)
+    return request.param
+
+
 @pytest.mark.gpu
-def test_gpu_matches_reference_golden():
+def test_gpu_matches_reference_golden(variant):
     from paper_2508_18588_b200.similarity import token_similarity_replay
     for case in load_golden("similarity.json.gz"):
         trace = _to_trace(_epochs(case))
@@ -69,7 +77,7 @@ def test_gpu_errors_like_reference():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", [0, 1, 2])
-def test_gpu_matches_oracle_random(seed):
+def test_gpu_matches_oracle_random(seed, variant):
     """Random small-vocabulary epochs (many collisions, ragged and tiny lengths)."""
     from paper_2508_18588_b200.similarity import token_similarity_replay
     rng = random.Random(seed)
@@ -92,7 +100,7 @@ def test_gpu_matches_oracle_random(seed):
 
 
 @pytest.mark.gpu
-def test_gpu_full_size_properties():
+def test_gpu_full_size_properties(variant):
     """configs[1]-sized epoch (64 prompts x 8 x 4096): identical epochs accept everything after
     the warm-up; a disjoint vocabulary accepts nothing; a shifted copy accepts all but warm-up."""
     import torch
