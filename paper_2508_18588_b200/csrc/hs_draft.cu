@@ -630,7 +630,8 @@ __global__ void k_inverse_sa(const int32_t* __restrict__ sa, int64_t n_suffix, i
 // ISA-seeded variant: after a run of `run` tokens matched by suffix h, suffix h + run shares the
 // next query's first p tokens, so its rank (isa) seeds the next search.  A gallop from that rank
 // brackets the insertion point within the p-gram's SA interval; a binary search finishes it.
-// Misses (run 0) fall back to a full search.
+// A miss (run 0) with a best match of l >= 1 tokens seeds the next search the same way with
+// h + 1 (sharing l - 1 tokens); only a miss with no shared token pays a full search.
 __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict__ isa, int32_t n_resp,
                                         const int32_t* __restrict__ tok, const int64_t* __restrict__ off,
                                         const int32_t* __restrict__ slot_of, int32_t p,
@@ -645,7 +646,8 @@ __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict
   const int64_t text_end = V.n_text + HS_TEXT_PAD - 1;
   int64_t acc = 0;
   if (S < E) {
-    int64_t hint = -1;   // SA index of a suffix sharing >= p tokens with the query, or -1
+    int64_t hint = -1;   // SA index of a suffix sharing >= hk tokens with the query, or -1
+    int32_t hk = 0;
     for (int32_t pos = p; pos < len;) {
       const int32_t* q = t + pos - p;
       const int32_t qn = len - pos + p;
@@ -654,7 +656,7 @@ __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict
       int order;
       if (hint >= 0) {
         const int32_t sp0 = V.sa[hint];
-        const int32_t l0 = lcp_query<1>(V.text, text_end, sp0, q, qn, p, &order);
+        const int32_t l0 = lcp_query<1>(V.text, text_end, sp0, q, qn, hk, &order);
         if (order < 0) {
           lo = hint + 1; l_lo = l0; sp_lo = sp0;
           for (int64_t step = 1;; step <<= 1) {
@@ -685,14 +687,14 @@ __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict
       }
       const int32_t best = max(l_lo, l_hi);
       const int32_t run = best - p;
-      if (run > 0) {
-        acc += run;
-        pos += run;
-        hint = isa[(l_lo >= l_hi ? sp_lo : sp_hi) + run];
-      } else {
-        pos += 1;
-        hint = -1;
-      }
+      // the next query is this one advanced by a tokens; the best suffix advanced by a shares
+      // best - a of them (any seed is correct -- the gallop only gets shorter with a good one)
+      const int32_t a = run > 0 ? run : 1;
+      const int32_t bsp = l_lo >= l_hi ? sp_lo : sp_hi;
+      if (run > 0) acc += run;
+      pos += a;
+      if (best >= a && bsp >= 0) { hint = isa[bsp + a]; hk = best - a; }   // -1 at a terminal
+      else { hint = -1; hk = 0; }
     }
   }
   if (lane == 0) accepted[r] = acc;
