@@ -329,17 +329,45 @@ def run_replay(args, dist, pk):
 
 # ------------------------------------------------------------------ rollout workload (headline)
 
-def derived_history(rng, truths, s, G, vocab):
-    """(D): G independent s-mutations (burst 4) of each prompt's current rollout; rewards Bernoulli(0.5)."""
+def derived_history(rng, truths, s, G, vocab, definition="D"):
+    """Synthetic previous-epoch history of each current rollout; rewards Bernoulli(0.5).
+
+    (D): the G members are independent s-mutations (burst 4) of the rollout itself.
+    (T): tracegen semantics (tracegen.py:123-162): the rollout is an s-mutation of member 0, and members
+         1..G-1 are siblings, s-mutations of member 0's parent -- built backwards from the rollout:
+         member 0 = mutate(rollout), parent = mutate(member 0), member g = mutate(parent)."""
     from paper_2508_18588_b200.synth import mutate
-    P, T = truths.shape
-    toks = np.empty((P, G, T), dtype=np.int32)
-    rew = np.empty((P, G), dtype=np.float64)
-    for p in range(P):
-        for g in range(G):
-            toks[p, g] = mutate(rng, truths[p].astype(np.int64), s, T, vocab, 4.0)
-            rew[p, g] = 1.0 if rng.random() < 0.5 else 0.0
+    n, T = truths.shape
+    toks = np.empty((n, G, T), dtype=np.int32)
+    rew = np.empty((n, G), dtype=np.float64)
+    for i in range(n):
+        truth = truths[i].astype(np.int64)
+        if definition == "D":
+            for g in range(G):
+                toks[i, g] = mutate(rng, truth, s, T, vocab, 4.0)
+                rew[i, g] = 1.0 if rng.random() < 0.5 else 0.0
+        else:
+            m0 = mutate(rng, truth, s, T, vocab, 4.0)
+            parent = mutate(rng, m0, s, T, vocab, 4.0)
+            toks[i, 0] = m0
+            rew[i, 0] = 1.0 if rng.random() < 0.5 else 0.0
+            for g in range(1, G):
+                toks[i, g] = mutate(rng, parent, s, T, vocab, 4.0)
+                rew[i, g] = 1.0 if rng.random() < 0.5 else 0.0
     return toks, rew
+
+
+def sample_prompts(prompt_of, pids, S, vocab):
+    """[len(pids) * S, P] prompts: sample j of prompt p ends with a sample-id token (vocab - 1 - j), so the S
+    greedy samples of a prompt are distinct sequences (hard part 7)."""
+    rows = []
+    for pid in pids:
+        base = prompt_of(pid)
+        for j in range(S):
+            r = base.copy()
+            r[-1] = vocab - 1 - j
+            rows.append(r)
+    return np.stack(rows).astype(np.int32)
 
 
 def cpu_rollout_sample(cfg, seed, prompts, T, s, G, threads, W=None):
@@ -366,6 +394,18 @@ def cpu_rollout_sample(cfg, seed, prompts, T, s, G, threads, W=None):
                       f"{threads} threads, prefill excluded"}, W
 
 
+def side_file(name, obj):
+    """Per-kernel detail that does not belong on the driver's one-line record (gpurun_out/ when present)."""
+    d = os.path.join(ROOT, "gpurun_out")
+    try:
+        os.makedirs(d, exist_ok=True)
+        with open(os.path.join(d, name), "w") as fh:
+            json.dump(obj, fh, indent=1)
+        return os.path.join("gpurun_out", name)
+    except OSError:
+        return None
+
+
 def run_rollout(args, dist, pk):
     import torch
     from paper_2508_18588_b200 import _lib
@@ -380,7 +420,8 @@ def run_rollout(args, dist, pk):
     dev = torch.device("cuda", dist.local)
     torch.cuda.set_device(dev)
     B, S, P, T, G = args.batch, args.samples, args.prompt_len, args.length, 8
-    n_prompts = B // S                  # prompts per rank per wave
+    per_wave = B // S                   # prompts per wave
+    n_waves = args.waves
     world, rank = dist.world, dist.rank
     w = Weights(cfg, dev, seed=args.seed)
     bcast_ms = None
@@ -392,65 +433,87 @@ def run_rollout(args, dist, pk):
             W.broadcast_weights(w, src=0)
             torch.cuda.synchronize()
             bcast_ms = 1e3 * (time.perf_counter() - t0)
-    eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev, attention=args.attention)
+    eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev, attention=args.attention,
+                        temperature=args.temperature, seed=args.seed)
 
     def prompt_tokens(pid):
         return np.random.default_rng([args.seed, 1000 + pid]).integers(0, cfg.vocab, size=P, dtype=np.int32)
 
-    # HistoPipe assignment over last-epoch medians (uniform 4k rollouts here -> ranked by id)
-    medians = {pid: float(T) for pid in range(n_prompts * world)}
+    def seq_keys(pids):
+        # sampling noise is keyed by a global sequence id (prompt, sample), not by the KV slot, so a sequence
+        # draws the same tokens on whichever rank / slot it runs
+        return np.array([pid * S + j for pid in pids for j in range(S)], dtype=np.int32)
+
+    # HistoPipe assignment over last-epoch medians (uniform lengths here -> ranked by id); every rank owns
+    # n_waves * per_wave prompts (weak scaling), rolled out one wave of B sequences at a time
+    medians = {pid: float(T) for pid in range(per_wave * n_waves * world)}
     mine1 = W.assign_prompts(medians, world, 1)[rank]
-    prompts1 = np.repeat(np.stack([prompt_tokens(p) for p in mine1]), S, axis=0)
-    # previous epoch (step 1): plain greedy rollout of the same engine (also the speculation-off baseline)
-    base = eng.rollout(prompts1, [T] * B, speculate=False)
-    nonspec_tps = B * T / (base.gpu_ms / 1e3)
-    # the same baseline with the other attention family: a run must keep one family (bit-exact spec ==
-    # greedy), but the fastest non-speculative configuration of the engine is the honest denominator
+    # previous epoch (step 1): plain rollouts of every wave (greedy, or T > 0 sampling with the same keys);
+    # they are the speculation-off baseline and the outputs the speculative step must reproduce bit for bit
+    outs, base_ms = {}, []
+    for wv in range(n_waves):
+        pids = mine1[wv * per_wave:(wv + 1) * per_wave]
+        res = eng.rollout(sample_prompts(prompt_tokens, pids, S, cfg.vocab), [T] * B, speculate=False,
+                          seq_keys=seq_keys(pids))
+        base_ms.append(res.gpu_ms)
+        for i, pid in enumerate(pids):
+            outs[pid] = res.tokens[i * S:(i + 1) * S]
+        if wv == 0:
+            base0 = res
+    # the same baseline with the other attention family on wave 0: a run must keep one family (bit-exact
+    # spec == plain), but the fastest non-speculative configuration of the engine is the honest denominator
     other = "mma_sync" if args.attention == "tcgen05" else "tcgen05"
     eng.attention = other
-    base_other = eng.rollout(prompts1, [T] * B, speculate=False)
+    base_other = eng.rollout(sample_prompts(prompt_tokens, mine1[:per_wave], S, cfg.vocab), [T] * B,
+                             speculate=False, seq_keys=seq_keys(mine1[:per_wave]))
     eng.attention = args.attention
-    nonspec_other_tps = B * T / (base_other.gpu_ms / 1e3)
     # epoch boundary: finished rollouts move to the rank owning the prompt at step 2 (all-to-all-v)
     owner2 = W.owner_map(W.assign_prompts(medians, world, 2))
-    recv = W.route_rollouts([(pid, base.tokens[i * S], 1.0) for i, pid in enumerate(mine1)], owner2, rank, world,
+    recv = W.route_rollouts([(pid, outs[pid].reshape(-1), 1.0) for pid in mine1], owner2, rank, world,
                             device=dev if world > 1 else "cpu")
     recv.sort(key=lambda r: r[0])
     mine2 = [r[0] for r in recv]
-    truths = np.stack([r[1] for r in recv])
+    truth_of = {r[0]: np.asarray(r[1], dtype=np.int32).reshape(S, T) for r in recv}
     rng = np.random.default_rng([args.seed, 2000 + rank])
-    hist, rew = derived_history(rng, truths, args.similarity, G, cfg.vocab)
-    prompts = np.repeat(np.stack([prompt_tokens(p) for p in mine2]), S, axis=0)
-    expect = np.repeat(truths, S, axis=0)
+    waves = []
+    resp_off = np.arange(B * G + 1, dtype=np.int64) * T
+    slot_resp_off = np.arange(B + 1, dtype=np.int64) * G
+    for wv in range(n_waves):
+        pids = mine2[wv * per_wave:(wv + 1) * per_wave]
+        expect = np.concatenate([truth_of[p] for p in pids])            # [B, T]
+        hist, rew = derived_history(rng, expect, args.similarity, G, cfg.vocab, args.history)
+        waves.append({"pids": pids, "expect": expect, "keys": seq_keys(pids),
+                      "h_prompts": torch.from_numpy(sample_prompts(prompt_tokens, pids, S, cfg.vocab)).pin_memory(),
+                      "h_hist": torch.from_numpy(hist.reshape(-1)).pin_memory(),
+                      "reward_fx": (rew.reshape(-1) * float(1 << 32)).astype(np.int64)})
     owner3 = W.owner_map(W.assign_prompts(medians, world, 3))
-    resp_off = np.arange(n_prompts * G + 1, dtype=np.int64) * T
-    slot_resp_off = np.arange(n_prompts + 1, dtype=np.int64) * G
-    reward_fx = (rew.reshape(-1) * float(1 << 32)).astype(np.int64)
-    h_prompts = torch.from_numpy(prompts).pin_memory()
-    h_hist = torch.from_numpy(hist.reshape(-1)).pin_memory()
     out_tok = torch.empty((B, T), dtype=torch.int32).pin_memory()
-    slots = np.arange(B) // S
+    slots = np.arange(B)                 # one history slot per sequence: its G previous-epoch relatives
     stream = torch.cuda.current_stream(dev)
-    acc = {"ms": [], "res": None, "exact": True, "route_ms": []}
+    acc = {"ms": [], "res": [], "exact": True, "route_ms": [], "n": 0, "ingest_ms": []}
 
     def step():
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d_prompts = h_prompts.to(dev, non_blocking=True)
-        d_hist = h_hist.to(dev, non_blocking=True)
+        wv = waves[acc["n"] % n_waves]
+        acc["n"] += 1
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        d_prompts = wv["h_prompts"].to(dev, non_blocking=True)
+        d_hist = wv["h_hist"].to(dev, non_blocking=True)
         e0.record(stream)
-        idx = GpuIndex.from_arrays(d_hist, resp_off, slot_resp_off, reward_fx)   # K1: ingest previous epoch
-        res = eng.rollout(d_prompts, [T] * B, slots=slots, index=idx, speculate=True)
+        idx = GpuIndex.from_arrays(d_hist, resp_off, slot_resp_off, wv["reward_fx"])   # K1: ingest the history
+        e2.record(stream)
+        res = eng.rollout(d_prompts, [T] * B, slots=slots, index=idx, speculate=True, seq_keys=wv["keys"])
         e1.record(stream)
         out_tok.copy_(torch.from_numpy(res.tokens))   # results already read back by rollout(); keep pinned copy
         e1.synchronize()
         # per-epoch history update: this step's rollouts go to their next owners
         t0 = time.perf_counter()
-        W.route_rollouts([(pid, res.tokens[i * S], 1.0) for i, pid in enumerate(mine2)], owner3, rank, world,
-                         device=dev if world > 1 else "cpu")
+        W.route_rollouts([(pid, res.tokens[i * S:(i + 1) * S].reshape(-1), 1.0) for i, pid in enumerate(wv["pids"])],
+                         owner3, rank, world, device=dev if world > 1 else "cpu")
         acc["route_ms"].append(1e3 * (time.perf_counter() - t0))
         acc["ms"].append(e0.elapsed_time(e1))
-        acc["res"] = res
-        acc["exact"] &= bool(np.array_equal(res.tokens, expect))
+        acc["ingest_ms"].append(e0.elapsed_time(e2))
+        acc["res"].append(res)
+        acc["exact"] &= bool(np.array_equal(res.tokens, wv["expect"]))
 
     lc0, mc0, gl0 = _lib.load().hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
     e2e_ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
@@ -458,8 +521,9 @@ def run_rollout(args, dist, pk):
                 + (eng.graph_launches - gl0)) // (args.steps + args.warmup)
     ms_dev = float(np.mean(acc["ms"][-args.steps:]))
     ms_dev = dist.max(ms_dev)
-    res = acc["res"]
-    st = res.stats.sum(axis=0)
+    timed_res = acc["res"][-args.steps:]
+    st = np.sum([r.stats.sum(axis=0) for r in timed_res], axis=0)
+    res = timed_res[-1]
     gen = B * T
     value = dist.sum(gen) / (ms_dev / 1e3)
     e2e = dist.sum(gen) / (e2e_ms / 1e3)
@@ -468,7 +532,7 @@ def run_rollout(args, dist, pk):
     t_roof = max(bytes_total / (pk["hbm_gbs"] * 1e9), res.flops / (pk["bf16_tflops_sustained"] * 1e12))
     # dominant kernel, timed live with CUDA events in a representative verify forward
     # verify-block sizes drawn from this run's own (sequence, iteration) histogram
-    qh = res.qlen_hist.astype(np.float64)
+    qh = np.sum([r.qlen_hist for r in timed_res], axis=0).astype(np.float64)
     q_lens = np.random.default_rng([args.seed, 77]).choice(len(qh), size=B, p=qh / qh.sum()).astype(np.int32)
     q_mean = float(q_lens.mean())
     prof, M = profile_forward(eng, B, P + T // 2, q_lens)
@@ -496,51 +560,59 @@ def run_rollout(args, dist, pk):
     std_cfg = (B, P, T, args.samples) == (1024, 256, 4096, 8) and dist.world == 1
     roof["traffic"], roof["traffic_source"] = measured_traffic("rollout:%s:%s" % (label, args.attention), std_cfg)
     roof["peak_source"] = pk["source"] + (" sustained" if roof["unit"] == "TFLOP/s" else "")
-    distinct = len({tuple(base.tokens[b, i:i + 4]) for b in range(0, B, S) for i in range(0, T - 4, 7)})
-    distinct /= max(1, len(range(0, B, S)) * len(range(0, T - 4, 7)))
+    bt = base0.tokens
+    grams = [tuple(bt[b, i:i + 4]) for b in range(0, B, max(1, B // 256)) for i in range(0, T - 4, 7)]
+    distinct = len(set(grams)) / max(1, len(grams))
+    side = side_file("bench_rollout_side_r%d.json" % rank, {
+        "kernels_ms_per_forward": kernels,
+        "profiled_forward": {"seqs": B, "rows_per_seq_mean": q_mean, "rows_per_seq_max": int(q_lens.max()),
+                             "ctx": P + T // 2, "M": M, "note": "verify-block sizes sampled from this run's histogram"},
+        "verify_rows_hist": {str(i): int(c) for i, c in enumerate(qh) if c},
+        "step_ms": acc["ms"], "ingest_ms": acc["ingest_ms"], "nonspec_wave_ms": base_ms,
+        "engine_iterations": [r.iterations for r in timed_res]})
+    sampling = args.temperature > 0
     line = {
-        "metric": "rollout tokens/sec (greedy HistoSpec: ingest + draft + verify forward + accept)",
+        "metric": "rollout tokens/sec (%s HistoSpec: ingest + draft + verify forward + accept)" % (
+            "rejection-sampling T=%g" % args.temperature if sampling else "greedy"),
         "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": e2e_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic prompts, random-init weights (seed %d), (D) history s=%.2f G=8" % (args.seed,
-                                                                                            args.similarity),
-        "config": {"workload": "configs[1]: %s, %d prompts x %d samples per wave (%d resident sequences), "
-                               "%d-token prompts, %d-token greedy rollouts, 1 wave per step" % (
-                                   cfg.name, n_prompts, S, B, P, T),
-                   "full_job": "512 prompts x 8 samples = %d waves of %d on 1 GPU" % (4096 // B, B),
+        "data": "synthetic prompts (sample-id token per sample), random-init weights (seed %d), (%s) history "
+                "s=%.2f G=%d per sequence" % (args.seed, args.history, args.similarity, G),
+        "config": {"workload": "configs[%d]: %s, %d prompts x %d samples per wave (%d resident sequences), "
+                               "%d-token prompts, %d-token %s rollouts, waves cycle over %d prompts per GPU" % (
+                                   2 if sampling else 1, cfg.name, per_wave, S, B, P, T,
+                                   "sampled" if sampling else "greedy", per_wave * n_waves),
+                   "step": "one wave: K1 ingest of its history + the HistoSpec rollout + routing of its outputs",
                    "parallelism": "dp%d (independent rollout workers)" % dist.world,
                    "l2": "KV cache (%.0f GB) and weights stream far beyond the 126 MB L2" % (
                        eng.cache.buf.numel() * 2 / 1e9)},
-        "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
-        "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
-        "acceptance_rate": float(st[2] / max(st[1], 1)),
-        "engine_iterations": res.iterations,
         "attention_family": args.attention,
-        "nonspec_value": dist.sum(B * T) / dist.max(base.gpu_ms / 1e3),
-        "nonspec_value_%s" % other: dist.sum(B * T) / dist.max(base_other.gpu_ms / 1e3),
-        "speedup_vs_nonspec": value / max(nonspec_tps, nonspec_other_tps, 1e-9) if dist.world == 1 else None,
-        "speedup_note": "vs the faster of the two attention families without speculation",
-        "bit_exact_vs_greedy": bool(dist.sum(float(acc["exact"])) == world),
         "collectives": {"weight_broadcast_ms": bcast_ms, "rollout_route_ms_per_step": float(np.mean(
             acc["route_ms"][-args.steps:])), "note": "epoch-boundary only: NCCL broadcast of the policy, "
-                                                     "all-to-all-v of finished rollouts to next-step owners "
-                                                     "(HistoPipe alternating assignment)"},
+                                                     "all-to-all-v of finished rollouts to next-step owners"},
+        "ingest_ms_per_step": float(np.mean(acc["ingest_ms"][-args.steps:])),
         "distinct_4gram_ratio": distinct,
-        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(h_prompts.numel() * 4 + h_hist.numel() * 4),
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(waves[0]["h_prompts"].numel() * 4
+                                                                            + waves[0]["h_hist"].numel() * 4),
                 "d2h_bytes_per_step": int(out_tok.numel() * 4 + B * 5 * 8)},
         "gpu_launches": int(launches),
         "roofline": roof,
-        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_wall_ms": ms_dev, "frac": t_roof * 1e3 / ms_dev,
-                          "flops": res.flops, "bytes": bytes_total, "note": "aggregate bound max(sum bytes/HBM, "
-                          "sum flops/sustained bf16) <= sum of per-forward maxima"},
-        "kernels_ms_per_forward": kernels,
-        "profiled_forward": {"seqs": B, "rows_per_seq_mean": q_mean, "rows_per_seq_max": int(q_lens.max()),
-                             "ctx": P + T // 2, "M": M,
-                             "note": "verify-block sizes sampled from this run's histogram"},
-        "verify_rows_hist": {str(i): int(c) for i, c in enumerate(res.qlen_hist) if c},
+        "roofline_step": {"t_roof_ms": t_roof * 1e3, "t_wall_ms": ms_dev, "frac": t_roof * 1e3 / ms_dev},
+        "side_file": side,
         "clocks": clocks,
+        # the speculation result last, where a truncated log tail still shows it
+        "nonspec_value_%s" % other: dist.sum(B * T) / dist.max(base_other.gpu_ms / 1e3),
+        "nonspec_value": dist.sum(B * T) / dist.max(float(np.mean(base_ms)) / 1e3),
+        "engine_iterations": float(np.mean([r.iterations for r in timed_res])),
+        "acceptance_rate": float(st[2] / max(st[1], 1)),
+        "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
+        "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
+        ("bit_exact_vs_plain_sampling" if sampling else "bit_exact_vs_greedy"):
+            bool(dist.sum(float(acc["exact"])) == world),
+        "speedup_vs_nonspec": value / max(dist.sum(B * T) / dist.max(float(np.mean(base_ms)) / 1e3),
+                                          dist.sum(B * T) / dist.max(base_other.gpu_ms / 1e3), 1e-9),
     }
-    return line, {"cfg": cfg, "prompts": prompts, "T": T, "w": w}
+    return line, {"cfg": cfg, "prompts": waves[0]["h_prompts"].numpy(), "T": T, "w": w}
 
 
 # ------------------------------------------------------------------ lookup microbenchmark
@@ -723,6 +795,9 @@ def main():
     ap.add_argument("--cpu-seqs", type=int, default=2)
     ap.add_argument("--cpu-tokens", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--waves", type=int, default=4, help="rollout: waves of --batch sequences per GPU (cycled)")
+    ap.add_argument("--history", default="D", choices=["D", "T"], help="similarity definition (SURVEY 8(d))")
+    ap.add_argument("--temperature", type=float, default=0.0, help="0: greedy verify; > 0: rejection sampling")
     ap.add_argument("--attention", default="tcgen05", choices=["tcgen05", "mma_sync"],
                     help="attention kernel family of the HistoSpec run (the baseline is measured with both)")
     args = ap.parse_args()

@@ -84,6 +84,7 @@ typedef struct {
   int64_t n_gram_groups;        /* host copy, valid after hs_index_build returns */
   void* ws;                     /* workspace pointer used by the build */
   size_t ws_bytes;
+  int32_t prefix_rounds;        /* prefix-doubling rounds the build ran (it stops once no tie can split) */
 } HsIndexView;
 
 typedef struct {
@@ -148,8 +149,11 @@ int hs_accept_replay(int32_t n_seq, const int32_t* d_truth, int32_t truth_stride
 
 /* K6 (greedy): truth = argmax rows of the verify forward.  Row q_off[s] + i
  * holds the model's next-token argmax after consuming [last, d_1..d_i].
- * Also rolls back kv_len[s] to prompt_len + gen_len_new - 1 (the bonus
- * token's KV is written by the next forward). */
+ * KV rollback is implicit: there is no kv_len array.  The next verify batch
+ * (hm_build_verify_batch) places its first row at position
+ * prompt_len + gen_len_new - 1, so KV rows written for rejected draft tokens
+ * lie past the valid context and are overwritten (the bonus token's KV is
+ * written by that next forward). */
 int hs_accept_greedy(int32_t n_seq, const int32_t* d_argmax, const int32_t* d_q_off,
                      const int32_t* d_target_len, const int32_t* d_draft_tok, int32_t draft_stride,
                      const int32_t* d_draft_len, const uint8_t* d_looked, const uint8_t* d_found,
@@ -167,7 +171,9 @@ int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int32_t* d_slo
 /* Token-similarity replay over an index of the previous epoch's responses:
  * response r (tokens d_tokens[d_resp_off[r] : d_resp_off[r+1]]) is replayed
  * against slot d_slot_of_resp[r]; d_accepted[r] = tokens accepted by the
- * prefix search (tracegen.py:306-353).  prefix_len < 1 -> HS_ERR_INVALID. */
+ * prefix search (tracegen.py:306-353).  A slot of -1 (or any slot outside
+ * [0, n_slots)) means "no history for this prompt": d_accepted[r] = 0, as in
+ * hs_draft / hs_lookup_batch.  prefix_len < 1 -> HS_ERR_INVALID. */
 int hs_similarity_replay(const HsIndexView* view, int32_t n_resp, const int32_t* d_tokens,
                          const int64_t* d_resp_off, const int32_t* d_slot_of_resp, int32_t prefix_len,
                          int64_t* d_accepted, hs_stream_t stream);

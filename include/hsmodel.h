@@ -115,6 +115,13 @@ int hm_attention(const void* d_q, const void* d_kcache, const void* d_vcache, in
 int hm_set_attention_family(int32_t family);
 int hm_attention_family(void);
 
+/* CTA caps of the persistent kernels launched after this call (process-wide, read at launch time, so a
+ * CUDA graph keeps the caps it was captured with): GEMMs use at most gemm_ctas CTAs and attention at most
+ * attn_ctas (0 = one per SM).  Two streams whose kernels' caps add up to the SM count run side by side,
+ * e.g. a KV-bandwidth-bound attention beside a tensor-core-bound GEMM of another half-batch.  A cap
+ * changes only which CTA computes a tile, never a tile's arithmetic (bits are unchanged). */
+int hm_set_grid_caps(int32_t gemm_ctas, int32_t attn_ctas);
+
 /* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent): the
  * per-sequence tile prefix and, for the tcgen05 family, each tile's sequence.  d_work holds
  * hm_attention_work_size(n_seq, max_q_len, H, KVH) int32 values. */
@@ -125,12 +132,38 @@ int hm_attention_plan(const int32_t* d_q_len, int32_t n_seq, int32_t max_q_len, 
 /* Verify-batch assembly for the rollout step: for each live sequence s
  * (gen_len < target_len) rows [last generated token, draft_1..draft_k] at
  * positions prompt_len[s] + gen_len[s] - 1 + i.  Writes q_off/q_len/pos0,
- * per-row token/position/slot, and the live row count to d_m[0]. */
+ * per-row token/position/slot, and the live row count to d_m[0].
+ * Optional accounting (NULL to skip), accumulated on the device:
+ *   d_acc[4] += {rows, 1 if rows > 0, sum over rows of (pos + 1), sum over live sequences of (pos0 + q)}
+ *   d_qhist[min(q, qhist_len - 1)] += 1 per sequence (q = 0 for finished ones), qhist_len in [2, 64].
+ * Optional row keys: d_row_key[row] = d_seq_key[s] (both NULL or both set) -- the per-row RNG key of
+ * hm_lm_head_sample, so sampling noise follows the sequence, not its KV slot. */
 int hm_build_verify_batch(int32_t n_seq, const int32_t* d_gen_tok, int32_t gen_stride, const int32_t* d_gen_len,
                           const int32_t* d_target_len, const int32_t* d_prompt_len, const int32_t* d_draft_tok,
                           int32_t draft_stride, const int32_t* d_draft_len, const int32_t* d_kv_slot,
                           int32_t* d_tokens, int32_t* d_pos, int32_t* d_row_slot, int32_t* d_q_off,
-                          int32_t* d_q_len, int32_t* d_pos0, int32_t* d_m, hm_stream_t stream);
+                          int32_t* d_q_len, int32_t* d_pos0, int32_t* d_m, int64_t* d_acc, int64_t* d_qhist,
+                          int32_t qhist_len, const int32_t* d_seq_key, int32_t* d_row_key, hm_stream_t stream);
+
+/* fp32 parity path (tests only): the same forward with fp32 operands, fp32
+ * accumulation and an fp32 KV cache ([slot][KVH][max_len][hd] float), plain SIMT kernels; weights are
+ * the bf16 tensors, widened on load.  Logits are held to 1e-3 relative of the fp32 restatement.
+ *   hm_f32_gemm:      Y[M, N] (+)= X[M, K] . W[N, K]^T (+ bias), W / bias bf16, X / Y fp32
+ *   hm_f32_rmsnorm:   out = x * rsqrt(mean(x^2) + eps) * w
+ *   hm_f32_rope_kv_append: rotate-half RoPE of q / k at pos[row]; q -> d_q [M][H][hd], k / v -> the caches
+ *   hm_f32_attention: causal GQA softmax attention of row m over keys 0..pos[m] of slot row_slot[m]
+ *   hm_f32_swiglu:    act = silu(gate) * up over the interleaved gate/up GEMM output (half-wide blocks) */
+int hm_f32_gemm(const float* d_x, int64_t ldx, const void* d_w, int64_t ldw, int32_t M, int32_t N, int32_t K,
+                const void* d_bias, float* d_y, int64_t ldy, int32_t accumulate, hm_stream_t stream);
+int hm_f32_rmsnorm(const float* d_x, const void* d_w, int32_t M, int32_t d, float eps, float* d_out,
+                   hm_stream_t stream);
+int hm_f32_rope_kv_append(const float* d_qkv, const int32_t* d_pos, const int32_t* d_row_slot, const float* d_cos,
+                          const float* d_sin, int32_t M, int32_t H, int32_t KVH, int32_t hd, float* d_q,
+                          float* d_kcache, float* d_vcache, int64_t slot_stride, int32_t max_len, hm_stream_t stream);
+int hm_f32_attention(const float* d_q, const float* d_kcache, const float* d_vcache, int64_t slot_stride,
+                     const int32_t* d_pos, const int32_t* d_row_slot, int32_t M, int32_t H, int32_t KVH, int32_t hd,
+                     int32_t max_len, float scale, float* d_out, hm_stream_t stream);
+int hm_f32_swiglu(const float* d_gu, int32_t M, int32_t F, int32_t half, float* d_act, hm_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -34,6 +34,7 @@ class HsIndexView(ctypes.Structure):
         ("n_slots", ctypes.c_int32), ("prefix_min", ctypes.c_int32), ("prefix_max", ctypes.c_int32),
         ("max_len", ctypes.c_int32), ("n_levels", ctypes.c_int32),
         ("n_gram_groups", ctypes.c_int64), ("ws", ctypes.c_void_p), ("ws_bytes", ctypes.c_size_t),
+        ("prefix_rounds", ctypes.c_int32),
     ]
 
 

@@ -24,6 +24,7 @@
 void hm_set_error(const char* msg);
 bool hm_make_tma_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 void hm_count_launches(int64_t n);
+int hm_cap(int n_sms, bool attn);
 
 namespace hm {
 
@@ -721,14 +722,14 @@ int launch_attn2(const void* d_q, const void* d_kcache, const void* d_vcache, in
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, k_attention2<HD, 2, 8>, 256, smem);
           if (occ8 < 1) occ8 = 1;
         }
-        k_attention2<HD, 2, 8><<<n_sm * occ8, 256, smem, st>>>(
+        k_attention2<HD, 2, 8><<<hm_cap(n_sm, true) * occ8, 256, smem, st>>>(
             (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
             d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
             mk, mv, use_tma, attn_flags());
         return 0;
       }
     }
-    k_attention2<HD, SL><<<n_sm * occupancy, 128, smem, st>>>(
+    k_attention2<HD, SL><<<hm_cap(n_sm, true) * occupancy, 128, smem, st>>>(
         (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_kcache, (const __nv_bfloat16*)d_vcache, slot_stride,
         d_q_off, d_q_len, d_pos0, d_kv_slot, H, KVH, q_rows, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq, d_work,
         mk, mv, use_tma, attn_flags());

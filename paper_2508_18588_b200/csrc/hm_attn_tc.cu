@@ -46,6 +46,7 @@
 
 void hm_set_error(const char* msg);
 void hm_count_launches(int64_t n);
+int hm_cap(int n_sms, bool attn);
 
 namespace hm {
 
@@ -780,7 +781,7 @@ int launch_attn_tc(const void* d_q, const int32_t* d_q_off, const int32_t* d_q_l
     cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);   // one CTA per SM (512 TMEM columns)
     if (getenv("HM_TC_GRID")) grid = atoi(getenv("HM_TC_GRID"));          // debugging only
   }
-  k_attn_tc<HD><<<grid, 320, TcAttn<HD>::SMEM, st>>>((const __nv_bfloat16*)d_q, d_q_off, d_q_len, d_pos0, d_kv_slot,
+  k_attn_tc<HD><<<hm_cap(grid, true), 320, TcAttn<HD>::SMEM, st>>>((const __nv_bfloat16*)d_q, d_q_off, d_q_len, d_pos0, d_kv_slot,
                                                       H, KVH, q_rows, max_len, scale_log2, (__nv_bfloat16*)d_out, n_seq,
                                                       d_work, mq, mk, mv, mk64, mv64);
   return 0;

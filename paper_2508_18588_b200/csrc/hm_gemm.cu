@@ -33,6 +33,7 @@
 
 void hm_set_error(const char* msg);
 void hm_count_launches(int64_t n);
+int hm_cap(int n_sms, bool attn);
 
 namespace hm {
 
@@ -88,10 +89,14 @@ __device__ __forceinline__ uint64_t mix_u64(uint64_t x) {
 __device__ __forceinline__ uint64_t gumbel_row_key(uint64_t seed, int k0, int k1) {
   return mix_u64(seed ^ mix_u64(((uint64_t)(uint32_t)k0 << 32) | (uint32_t)k1));
 }
+// u from the top 23 bits: (k + 0.5) * 2^-23, k < 2^23, is exact in fp32 and lies in [2^-24, 1 - 2^-24], so
+// it never rounds to 0 or 1 (a 32-bit h converted to float rounds to 2^32 for the top 128 values, giving
+// u = 1 and an infinite Gumbel value that wins the argmax).  The inner log is the accurate logf: near u = 1,
+// -log(u) ~ 1 - u is tiny and __logf's absolute error could make it <= 0 (NaN / inf after the outer log).
 __device__ __forceinline__ float gumbel(uint64_t rkey, int v) {
-  const uint32_t h = (uint32_t)(mix_u64(rkey + (uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ULL) >> 32);
-  const float u = ((float)h + 0.5f) * 2.3283064365386963e-10f;   // (0, 1)
-  return -__logf(-__logf(u));
+  const uint32_t h = (uint32_t)(mix_u64(rkey + (uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ULL) >> 41);
+  const float u = ((float)h + 0.5f) * 1.1920928955078125e-07f;   // [2^-24, 1 - 2^-24]
+  return -__logf(-logf(u));
 }
 
 template <int BN, int kStages>
@@ -458,7 +463,8 @@ int launch(const CUtensorMap& mx, const CUtensorMap& mw, const hm::EpiParams& p,
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = ((p.M + hm::BM - 1) / hm::BM) * ((p.N + BN - 1) / BN);
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int cap = hm_cap(g_num_sms, false);
+  const int grid = tiles < cap ? tiles : cap;
   hm_count_launches(1);
   kern<<<grid, hm::kThreads, C::kSmemBytes, st>>>(mx, mw, p);
   cudaError_t e = cudaGetLastError();

@@ -16,6 +16,19 @@ void hm_count_launches(int64_t n) { __atomic_fetch_add(&g_launches, n, __ATOMIC_
 extern "C" const char* hm_last_error(void) { return g_err; }
 extern "C" int64_t hm_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
+// persistent-kernel CTA caps (hm_set_grid_caps); 0 = one CTA per SM
+int g_cap_gemm = 0, g_cap_attn = 0;
+extern "C" int hm_set_grid_caps(int32_t gemm_ctas, int32_t attn_ctas) {
+  if (gemm_ctas < 0 || attn_ctas < 0) { hm_set_error("hm_set_grid_caps: caps must be >= 0"); return HM_ERR_INVALID; }
+  g_cap_gemm = gemm_ctas;
+  g_cap_attn = attn_ctas;
+  return HM_OK;
+}
+int hm_cap(int n_sms, bool attn) {
+  const int c = attn ? g_cap_attn : g_cap_gemm;
+  return (c > 0 && c < n_sms) ? c : n_sms;
+}
+
 #define HM_LAUNCH_CHECK()                                 \
   do {                                                    \
     hm_count_launches(1);                                 \
@@ -183,11 +196,21 @@ __global__ void k_build_verify(int n_seq, const int32_t* __restrict__ gen_tok, i
                                int draft_stride, const int32_t* __restrict__ draft_len,
                                const int32_t* __restrict__ kv_slot, int32_t* __restrict__ tokens,
                                int32_t* __restrict__ pos, int32_t* __restrict__ row_slot, int32_t* __restrict__ q_off,
-                               int32_t* __restrict__ q_len, int32_t* __restrict__ pos0, int32_t* __restrict__ m_out) {
+                               int32_t* __restrict__ q_len, int32_t* __restrict__ pos0, int32_t* __restrict__ m_out,
+                               long long* __restrict__ acc, long long* __restrict__ qhist, int qhist_len,
+                               const int32_t* __restrict__ seq_key, int32_t* __restrict__ row_key) {
   __shared__ int warp_sums[32];
   __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
+  __shared__ unsigned long long s_rows_pos, s_ctx;   // sum over rows of (pos + 1); over live seqs of ctx + q
+  __shared__ unsigned int s_hist[64];
+  if (threadIdx.x == 0) {
+    carry = 0;
+    s_rows_pos = 0;
+    s_ctx = 0;
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
+  unsigned long long my_rows_pos = 0, my_ctx = 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int base = 0; base < n_seq; base += blockDim.x) {
     const int s = base + threadIdx.x;
@@ -227,13 +250,35 @@ __global__ void k_build_verify(int n_seq, const int32_t* __restrict__ gen_tok, i
         tokens[off + i] = i == 0 ? gen_tok[(size_t)s * gen_stride + g - 1] : draft_tok[(size_t)s * draft_stride + i - 1];
         pos[off + i] = p0 + i;
         row_slot[off + i] = kv_slot[s];
+        if (row_key) row_key[off + i] = seq_key[s];
       }
+      if (q > 0) {
+        // flop / KV-byte accounting of the forward (integers: order independent)
+        my_rows_pos += (unsigned long long)q * (unsigned long long)(p0 + 1) + (unsigned long long)q * (q - 1) / 2;
+        my_ctx += (unsigned long long)(p0 + q);
+      }
+      if (qhist) atomicAdd(&s_hist[q < qhist_len - 1 ? q : qhist_len - 1], 1u);
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = off + q;
     __syncthreads();
   }
-  if (threadIdx.x == 0) m_out[0] = carry;
+  if (acc) {
+    atomicAdd(&s_rows_pos, my_rows_pos);
+    atomicAdd(&s_ctx, my_ctx);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m_out[0] = carry;
+    if (acc) {   // [rows, iterations with rows, sum (pos + 1) over rows, sum (ctx + q) over live sequences]
+      acc[0] += carry;
+      acc[1] += carry > 0;
+      acc[2] += (long long)s_rows_pos;
+      acc[3] += (long long)s_ctx;
+    }
+  }
+  if (qhist)
+    for (int i = threadIdx.x; i < qhist_len; i += blockDim.x) qhist[i] += s_hist[i];
 }
 
 }  // namespace hm
@@ -297,12 +342,23 @@ extern "C" int hm_build_verify_batch(int32_t n_seq, const int32_t* d_gen_tok, in
                                      const int32_t* d_prompt_len, const int32_t* d_draft_tok, int32_t draft_stride,
                                      const int32_t* d_draft_len, const int32_t* d_kv_slot, int32_t* d_tokens,
                                      int32_t* d_pos, int32_t* d_row_slot, int32_t* d_q_off, int32_t* d_q_len,
-                                     int32_t* d_pos0, int32_t* d_m, hm_stream_t stream) {
+                                     int32_t* d_pos0, int32_t* d_m, int64_t* d_acc, int64_t* d_qhist,
+                                     int32_t qhist_len, const int32_t* d_seq_key, int32_t* d_row_key,
+                                     hm_stream_t stream) {
   if (n_seq <= 0) return HM_OK;
+  if ((d_seq_key == nullptr) != (d_row_key == nullptr)) {
+    hm_set_error("hm_build_verify_batch: d_seq_key and d_row_key go together");
+    return HM_ERR_INVALID;
+  }
+  if (d_qhist && (qhist_len < 2 || qhist_len > 64)) {
+    hm_set_error("hm_build_verify_batch: qhist_len must be in [2, 64]");
+    return HM_ERR_INVALID;
+  }
   hm::k_build_verify<<<1, 1024, 0, (cudaStream_t)stream>>>(n_seq, d_gen_tok, gen_stride, d_gen_len, d_target_len,
                                                            d_prompt_len, d_draft_tok, draft_stride, d_draft_len,
                                                            d_kv_slot, d_tokens, d_pos, d_row_slot, d_q_off, d_q_len,
-                                                           d_pos0, d_m);
+                                                           d_pos0, d_m, (long long*)d_acc, (long long*)d_qhist,
+                                                           qhist_len, d_seq_key, d_row_key);
   HM_LAUNCH_CHECK();
   return HM_OK;
 }

@@ -568,6 +568,10 @@ __global__ void k_similarity_replay(HsIndexView V, int32_t n_resp, const int32_t
   const int32_t* t = tok + off[r];
   const int32_t len = (int32_t)(off[r + 1] - off[r]);
   const int32_t slot = slot_of[r];
+  if (slot < 0 || slot >= V.n_slots) {   // -1 = no history for this prompt (the C-ABI's convention)
+    if (lane_id() == 0) accepted[r] = 0;
+    return;
+  }
   const int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
   const int64_t text_end = V.n_text + HS_TEXT_PAD - 1;
   int64_t acc = 0;
@@ -642,6 +646,10 @@ __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict
   const int32_t* t = tok + off[r];
   const int32_t len = (int32_t)(off[r + 1] - off[r]);
   const int32_t slot = slot_of[r];
+  if (slot < 0 || slot >= V.n_slots) {   // -1 = no history for this prompt (the C-ABI's convention)
+    if (lane_id() == 0) accepted[r] = 0;
+    return;
+  }
   const int64_t S = V.slot_sa_off[slot], E = V.slot_sa_off[slot + 1];
   const int64_t text_end = V.n_text + HS_TEXT_PAD - 1;
   int64_t acc = 0;

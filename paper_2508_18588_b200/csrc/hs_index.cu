@@ -74,6 +74,16 @@ __global__ void k_scatter_rank(const int32_t* __restrict__ sa, const int32_t* __
   rank[sa[k]] = gstart[k] + 1;
 }
 
+// Prefix doubling has converged after a round with window w when no group of equal w-windows can still
+// split: every suffix that is not its group's head (so it ties with its predecessor) already has the
+// terminal inside its window (rem < w) -- tied windows that end at a terminal stay tied forever.
+__global__ void k_converged(const int32_t* __restrict__ sa, const int32_t* __restrict__ gstart,
+                            const int32_t* __restrict__ rem, int64_t n, int64_t w, unsigned long long* flag) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (gstart[k] != (int32_t)k && rem[sa[k]] >= w) *flag = 1ull;
+}
+
 __global__ void k_double_keys(const int32_t* __restrict__ sufpos, const int32_t* __restrict__ rank,
                               const int32_t* __restrict__ rem, int64_t n, int32_t h, int32_t bits,
                               uint64_t* __restrict__ keys) {
@@ -613,6 +623,7 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
   view->table = nullptr;
   view->table_mask = 0;
   view->n_gram_groups = 0;
+  view->prefix_rounds = 0;
   view->ws = d_ws;
   view->ws_bytes = ws_bytes;
   if (n == 0) {
@@ -640,8 +651,22 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
     k_scatter_rank<<<blocks(n), 256, 0, st>>>(dv.Current(), L.gstart, n, rank_ptrs[0]);
     HS_CUDA_TRY(cudaMemcpyAsync(L.sa, dv.Current(), sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
   }
-  // suffix positions in text order for key generation (values are text positions)
+  // suffix positions in text order for key generation (values are text positions).  Round j doubles the
+  // window to 2^(j+1); once no tie can split any more the remaining rounds are skipped (one flag read per
+  // round: a few microseconds against a full radix sort), and the LCP descent starts at the last level built
+  unsigned long long* conv_flag = L.counters + n_slots + 1;
+  int levels_built = 0;
   for (int j = 0; j < d.rounds; ++j) {
+    if (j > 0) {
+      unsigned long long not_done = 1;
+      HS_CUDA_TRY(cudaMemsetAsync(conv_flag, 0, sizeof(unsigned long long), st));
+      hs_count_launches(1);
+      k_converged<<<blocks(n), 256, 0, st>>>(L.sa, L.gstart, L.rem, n, (int64_t)1 << j, conv_flag);
+      HS_CUDA_TRY(cudaMemcpyAsync(&not_done, conv_flag, sizeof(not_done), cudaMemcpyDeviceToHost, st));
+      HS_CUDA_TRY(cudaStreamSynchronize(st));
+      if (!not_done) break;
+    }
+    levels_built = j + 1;
     int32_t h = 1 << j;
     // keys from the previous order (any order works; reuse sa to keep locality)
     hs_count_launches(1);
@@ -661,7 +686,8 @@ extern "C" int hs_index_build(const int32_t* d_tokens, int64_t n_tokens, const i
 
   // ---- LCP, weights, sparse table
   hs_count_launches(1);
-  k_lcp<<<blocks(n + 1), 256, 0, st>>>(L.sa, L.rem, L.rid, L.resp_slot, L.rank_ptrs, d.rounds, n, L.lcp);
+  k_lcp<<<blocks(n + 1), 256, 0, st>>>(L.sa, L.rem, L.rid, L.resp_slot, L.rank_ptrs, levels_built, n, L.lcp);
+  view->prefix_rounds = levels_built;
   hs_count_launches(1);
   k_weights<<<blocks(n + 1), 256, 0, st>>>(L.sa, L.rid, L.reward, n, L.wtmp);
   HS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cub_bytes, L.wtmp, L.wsum, (int)(n + 1), st));

@@ -74,6 +74,7 @@ class RolloutEngine:
         self.tokens = torch.empty(R, **i32)
         self.pos = torch.empty(R, **i32)
         self.row_slot = torch.empty(R, **i32)
+        self.row_key = torch.empty(R, **i32)     # per-row sampling key: the row's sequence key
         self.q_off = torch.empty(n_slots, **i32)
         self.q_len = torch.empty(n_slots, **i32)
         self.pos0 = torch.empty(n_slots, **i32)
@@ -81,7 +82,7 @@ class RolloutEngine:
         self.kv_slot = torch.arange(n_slots, **i32)
 
     # -------------------------------------------------------------- phases
-    def prefill(self, prompts, state: SpecBatch):
+    def prefill(self, prompts, state: SpecBatch, seq_key=None):
         """Prompt forward in chunks; the last prompt row's argmax is response token 0."""
         import torch
         B, P = prompts.shape
@@ -95,11 +96,12 @@ class RolloutEngine:
             self.tokens[:M] = prompts[a:b].reshape(-1)
             self.pos[:M] = torch.arange(P, dtype=torch.int32, device=self.device).repeat(n)
             self.row_slot[:M] = self.kv_slot[a:b].repeat_interleave(P)
+            self.row_key[:M] = (seq_key if seq_key is not None else self.kv_slot)[a:b].repeat_interleave(P)
             self.q_off[:n] = torch.arange(n, dtype=torch.int32, device=self.device) * P
             self.q_len[:n] = P
             self.pos0[:n] = 0
             am = self.fwd.run(M, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
-                              self.kv_slot[a:b], n, P)
+                              self.kv_slot[a:b], n, P, row_key=self.row_key)
             first[a:b] = am.view(n, P)[:, P - 1]
             rows += M
         # iteration 0 of every response: a plain decode (pos 0 < prefix length)
@@ -110,10 +112,12 @@ class RolloutEngine:
         return rows
 
     def rollout(self, prompts, target_len, slots=None, index=None, speculate=True, record_tpi=False,
-                recent_acceptance=None):
+                recent_acceptance=None, seq_keys=None):
         """Generate target_len[b] tokens for each prompt row b (greedy), drafting from `index`.
 
         prompts: [B, P] int32 (host numpy or device tensor); slots[b]: history slot of b in index.
+        seq_keys[b]: the sampling key of sequence b (T > 0; default b), so a sequence's samples do not
+        depend on the batch row or KV slot it runs in.
         recent_acceptance: the worker's cumulative acceptance rate; when given, the batch gate
         decides whether this batch speculates at all (spec_engine.gate_check, as sim.py:346-352).
         """
@@ -137,19 +141,17 @@ class RolloutEngine:
         state = SpecBatch(slots, tl, self.spec, speculate=np.full(B, int(spec_on), np.uint8), device=self.device,
                           max_len=int(tl.max()), record_tpi=record_tpi)
         prompt_len = torch.full((B,), P, dtype=torch.int32, device=self.device)
+        seq_key = torch.as_tensor(np.arange(B, dtype=np.int32) if seq_keys is None
+                                  else np.asarray(seq_keys, dtype=np.int32)).to(self.device)
         st = torch.cuda.current_stream(self.device)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         L = lib()
         ev0.record(st)
-        rows = self.prefill(prompts, state)
-        # device-side counters: rows, iterations, sum over rows of (pos + 1), over sequences of (ctx + q)
-        acc = torch.zeros(4, dtype=torch.int64, device=self.device)
-        acc[0] = 0
-        acc[2] = B * P * (P + 1) // 2
-        acc[3] = B * P
-        row_ids = torch.arange(self.fwd.max_rows, dtype=torch.int32, device=self.device)
+        rows = self.prefill(prompts, state, seq_key)
+        # device-side counters (accumulated by hm_build_verify_batch): rows, iterations, sum over rows of
+        # (pos + 1), over sequences of (ctx + q); prefill rows are added here
+        acc = torch.tensor([0, 0, B * P * (P + 1) // 2, B * P], dtype=torch.int64, device=self.device)
         qhist = torch.zeros(self.max_q + 1, dtype=torch.int64, device=self.device)
-        ones = torch.ones(B, dtype=torch.int64, device=self.device)
         # launch geometry of the captured iteration: one row per sequence without speculation (decode-sized
         # GEMM tiles and attention tiles), up to 1 + window rows per sequence with it
         q_cap = self.max_q if spec_on else 1
@@ -165,16 +167,10 @@ class RolloutEngine:
                 prompt_len.data_ptr(), state.draft_tok.data_ptr(), state.draft_tok.shape[1],
                 state.draft_len.data_ptr(), self.kv_slot.data_ptr(), self.tokens.data_ptr(), self.pos.data_ptr(),
                 self.row_slot.data_ptr(), self.q_off.data_ptr(), self.q_len.data_ptr(), self.pos0.data_ptr(),
-                self.d_m.data_ptr(), s.cuda_stream))
-            m = self.d_m[0]
-            live = row_ids[:R] < m
-            acc[0] += m
-            acc[1] += (m > 0).to(torch.int64)
-            acc[2] += torch.where(live, self.pos[:R].to(torch.int64) + 1, 0).sum()
-            acc[3] += ((self.pos0[:B].to(torch.int64) + self.q_len[:B]) * (self.q_len[:B] > 0)).sum()
-            qhist.index_add_(0, self.q_len[:B].to(torch.int64), ones)
+                self.d_m.data_ptr(), acc.data_ptr(), qhist.data_ptr(), qhist.numel(), seq_key.data_ptr(),
+                self.row_key.data_ptr(), s.cuda_stream))
             am = self.fwd.run(R, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
-                              self.kv_slot, B, q_cap, stream=s, m_dev=self.d_m)
+                              self.kv_slot, B, q_cap, stream=s, m_dev=self.d_m, row_key=self.row_key)
             state.accept_greedy(am, self.q_off, s)
 
         # first decode iteration eagerly (initializes kernel attributes), then replay a captured graph

@@ -25,10 +25,17 @@ from . import _lib
 from .index import GpuIndex
 
 
-# "isa" (default, 2.0x faster on the configs[1] epoch): ISA-seeded searches (hs_similarity_replay_isa);
-# anything else: plain searches
-# (hs_similarity_replay, whose kernel family HS_SIM_VARIANT also selects in the library)
-_VARIANT = os.environ.get("HS_SIM_VARIANT", "isa")
+# HS_SIM_SEARCH = "isa" (default, 2.0x faster on the configs[1] epoch): ISA-seeded searches
+# (hs_similarity_replay_isa); "plain": plain binary searches (hs_similarity_replay, whose kernel variant the
+# library's own A/B switch HS_SIM_VARIANT selects).  Any other value is an error, not a silent fallback.
+_SEARCHES = ("isa", "plain")
+
+
+def _search_mode() -> str:
+    mode = os.environ.get("HS_SIM_SEARCH", "isa")
+    if mode not in _SEARCHES:
+        raise ValueError(f"HS_SIM_SEARCH must be one of {_SEARCHES}, got {mode!r}")
+    return mode
 
 
 @dataclass(frozen=True)
@@ -70,18 +77,26 @@ def replay_against_index(index: GpuIndex, d_tokens, resp_off, slot_of_resp, pref
     torch = _lib.require_cuda()
     if prefix_len < 1:
         raise ValueError("prefix_len must be >= 1")        # tracegen.py:322-323
+    mode = _search_mode()
     n = int(slot_of_resp.numel())
     dev = d_tokens.device
     s = stream if stream is not None else torch.cuda.current_stream(dev)
-    out = torch.zeros(n, dtype=torch.int64, device=dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
-        if _VARIANT == "isa":
-            isa = getattr(index, "_isa", None)
-            if isa is None:
+    with torch.cuda.device(dev), torch.cuda.stream(s):
+        # allocated on s (the kernel writes every entry), so no fill on another stream can race it
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+        if mode == "isa":
+            cached = getattr(index, "_isa", None)
+            if cached is None:
                 isa = torch.empty(max(1, index.view.n_text), dtype=torch.int32, device=dev)
                 _lib.check(lib.hs_index_inverse_sa(ctypes.byref(index.view), isa.data_ptr(), s.cuda_stream))
-                index._isa = isa      # 4 B per indexed token, kept with the index
+                ready = torch.cuda.Event()
+                ready.record(s)
+                index._isa = (isa, ready)      # 4 B per indexed token, kept with the index
+            else:
+                # built on another stream by an earlier call: order this stream after the build
+                isa, ready = cached
+                s.wait_event(ready)
             _lib.check(lib.hs_similarity_replay_isa(
                 ctypes.byref(index.view), isa.data_ptr(), n, d_tokens.data_ptr(), resp_off.data_ptr(),
                 slot_of_resp.data_ptr(), int(prefix_len), out.data_ptr(), s.cuda_stream))

@@ -342,6 +342,33 @@ def test_gumbel_sampling_marginal_matches_softmax(torch):
     assert torch.equal(out2, out[sub])
 
 
+def test_gumbel_sampling_large_vocab_no_spurious_winners(torch):
+    """V = 151,936 (the Qwen head): one dominant logit (+20 over 0) loses with probability
+    (V - 1) e^-20 / (1 + (V - 1) e^-20) = 3.1e-4 per row, i.e. ~2.6 of 8,192 rows.  A Gumbel uniform that
+    rounds to 0 or 1 gives an infinite noise value that beats any logit, so a random token wins; with 32-bit
+    uniforms that happens on ~0.45% of rows (~37 here).  Every per-tile partial must also be finite."""
+    import paper_2508_18588_b200.model as Mo
+    K, V, n = 64, 151936, 8192
+    x = torch.zeros(n, K, dtype=torch.bfloat16, device="cuda")
+    x[:, 0] = 1.0
+    E = torch.zeros(V, K, dtype=torch.bfloat16, device="cuda")
+    hot = 12345
+    E[hot, 0] = 20.0
+    key0 = torch.arange(n, dtype=torch.int32, device="cuda")
+    key1 = torch.full((n,), 3, dtype=torch.int32, device="cuda")
+    nt = V // 128
+    av = torch.empty(n, nt, device="cuda")
+    ai = torch.empty(n, nt, dtype=torch.int32, device="cuda")
+    L = Mo.lib()
+    Mo.check(L.hm_lm_head_sample(x.data_ptr(), K, E.data_ptr(), K, n, V, K, key0.data_ptr(), key1.data_ptr(), 77,
+                                 1.0, av.data_ptr(), ai.data_ptr(), None, 0))
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    Mo.check(L.hm_argmax_reduce(av.data_ptr(), ai.data_ptr(), n, nt, None, out.data_ptr(), 0))
+    assert torch.isfinite(av).all()
+    misses = int((out != hot).sum())
+    assert misses <= 12, misses     # Poisson(2.6): P(> 12) ~ 1e-5
+
+
 def test_tiny_engine_rejection_sampling_spec_equals_plain_sampling(torch):
     """T = 1.0: HistoSpec output == plain sampling output with the same seed (Gumbel-max coupling),
     and the accept profile == reference state machine on that output."""

@@ -47,12 +47,19 @@ def _to_trace(tr):
     return {e: {pid: [(t, 0.0) for t in rs] for pid, rs in d.items()} for e, d in tr.items()}
 
 
-@pytest.fixture(params=["isa", "u1"])
+@pytest.fixture(params=["isa", "plain"])
 def variant(request, monkeypatch):
-    """Both search kernels: ISA-seeded (default) and plain binary search."""
-    from paper_2508_18588_b200 import similarity
-    monkeypatch.setattr(similarity, "_VARIANT", request.param)
+    """Both search kernels: ISA-seeded (default) and plain binary search (HS_SIM_SEARCH)."""
+    monkeypatch.setenv("HS_SIM_SEARCH", request.param)
     return request.param
+
+
+def test_unknown_search_mode_is_an_error(monkeypatch):
+    """A typo in HS_SIM_SEARCH raises instead of silently selecting the slower kernel."""
+    from paper_2508_18588_b200 import similarity
+    monkeypatch.setenv("HS_SIM_SEARCH", "ISA")
+    with pytest.raises(ValueError):
+        similarity._search_mode()
 
 
 @pytest.mark.gpu
