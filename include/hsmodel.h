@@ -59,6 +59,11 @@ int hm_lm_head_sample(const void* d_x, int64_t ldx, const void* d_w, int64_t ldw
 /* GEMM tile width chosen for an N (a function of N only, never of M). */
 int hm_gemm_bn(int32_t n);
 
+/* CTA-pair (cta_group::2, 256 x 256 tile over two SMs) GEMM kernels: 1 = used when there are at least
+ * (#SMs / 2) 256 x 256 tiles (default), 0 = never (1-CTA kernels only).  Same bits either way; a switch for
+ * A/B timing and the bit-neutrality tests. */
+int hm_set_gemm_pair(int32_t on);
+
 /* LM-head argmax: reduce the [M, n_tiles] partials of HM_EPI_ARGMAX (ties -> smallest id). */
 int hm_argmax_reduce(const float* d_val, const int32_t* d_idx, int32_t M, int32_t n_tiles, const int32_t* d_m,
                      int32_t* d_out, hm_stream_t stream);

@@ -251,6 +251,11 @@ def profile_forward(engine: RolloutEngine, B: int, ctx: int, q, launch_rows=None
         m_dev = torch.tensor([M], **i32)
     engine.fwd.run(R, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qcap, m_dev=m_dev)   # warm
     prof = []
+    # hold the stream with a ~50 ms spin so the host enqueues every launch (and its events) before the first
+    # one runs: the kernels then run back to back, as in the engine's CUDA graphs, and no event interval
+    # includes the host's per-launch cost
+    torch.cuda.synchronize(dev)
+    torch.cuda._sleep(100_000_000)
     engine.fwd.run(R, tokens, pos, row_slot, q_off, q_len, pos0, kv, B, qcap, m_dev=m_dev, prof=prof)
     torch.cuda.synchronize(dev)
     out = {}

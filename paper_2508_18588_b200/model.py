@@ -45,6 +45,7 @@ SIGNATURES = {
     "hm_attention_work_size": [_I32, _I32, _I32, _I32],
     "hm_set_attention_family": [_I32],
     "hm_set_grid_caps": [_I32, _I32],
+    "hm_set_gemm_pair": [_I32],
     "hm_f32_gemm": [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _I32, _P],
     "hm_f32_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P],
     "hm_f32_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P],

@@ -92,6 +92,56 @@ def test_gemm_tile_width_is_bit_neutral(torch, epi, N):
     assert torch.equal(small, large[:100])
 
 
+@pytest.mark.parametrize("epi,N,K,M", [(0, 2048, 1536, 5110), (4, 1536, 1536, 4999), (4, 1536, 8960, 5110),
+                                       (1, 17920, 1536, 1111), (3, 38016, 1536, 700), (2, 1536, 1536, 4737)])
+def test_gemm_pair_is_bit_neutral(torch, epi, N, K, M):
+    """The CTA-pair kernel (cta_group::2, 256 x 256 tiles over two SMs) gives every row the same bits as the
+    1-CTA kernels, and matches fp32 torch; ragged M leaves the last pair tile (and whole peer CTAs) part-empty."""
+    import paper_2508_18588_b200.model as Mo
+    L = Mo.lib()
+    g = torch.Generator(device="cuda").manual_seed(N + K + epi)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g).to(torch.bfloat16)
+    r0 = torch.randn(M, N, device="cuda", generator=g) if epi == 2 else None
+
+    def run():
+        if epi in (0, 1):
+            o = torch.zeros(M, N if epi == 0 else N // 2, dtype=torch.bfloat16, device="cuda")
+            _gemm(M, epi, x, w, bias=b if epi == 0 else None, out=o)
+            return (o,)
+        if epi in (2, 4):
+            o = r0.clone() if epi == 2 else torch.zeros(M, N, dtype=torch.float32, device="cuda")
+            _gemm(M, epi, x, w, resid=o)
+            return (o,)
+        av = torch.zeros(M, N // 128, dtype=torch.float32, device="cuda")
+        ai = torch.zeros(M, N // 128, dtype=torch.int32, device="cuda")
+        _gemm(M, 3, x, w, amax=(av, ai))
+        return av, ai
+
+    try:
+        Mo.check(L.hm_set_gemm_pair(1))
+        paired = run()
+        Mo.check(L.hm_set_gemm_pair(0))
+        single = run()
+    finally:
+        Mo.check(L.hm_set_gemm_pair(1))
+    for a, c in zip(paired, single):
+        assert torch.equal(a, c)
+    ref = x.float() @ w.float().T
+    if epi == 0:
+        ref = ref + b.float()
+        assert ((paired[0].float() - ref).abs() <= ref.abs() * 2 ** -7 + 1e-3).all()
+    elif epi == 4:
+        assert torch.allclose(paired[0], ref, rtol=1e-4, atol=1e-3)
+    elif epi == 2:
+        assert torch.allclose(paired[0], r0 + ref, rtol=1e-4, atol=1e-3)
+    elif epi == 3:
+        assert torch.equal(paired[1].view(M, -1, 1)[:, :, 0] // 128, torch.arange(N // 128, device="cuda").expand(M, -1))
+        best = ref.view(M, N // 128, 128).max(dim=2).values
+        assert torch.allclose(paired[0], best, rtol=1e-4, atol=1e-3)
+
+
 def test_gemm_swiglu_residual_argmax(torch):
     from paper_2508_18588_b200.model import interleave_gate_up
     g = torch.Generator(device="cuda").manual_seed(5)
