@@ -467,53 +467,100 @@ def run_rollout(args, dist, pk):
     base_other = eng.rollout(sample_prompts(prompt_tokens, mine1[:per_wave], S, cfg.vocab), [T] * B,
                              speculate=False, seq_keys=seq_keys(mine1[:per_wave]))
     eng.attention = args.attention
-    # epoch boundary: finished rollouts move to the rank owning the prompt at step 2 (all-to-all-v)
-    owner2 = W.owner_map(W.assign_prompts(medians, world, 2))
-    recv = W.route_rollouts([(pid, outs[pid].reshape(-1), 1.0) for pid in mine1], owner2, rank, world,
-                            device=dev if world > 1 else "cpu")
-    recv.sort(key=lambda r: r[0])
-    mine2 = [r[0] for r in recv]
-    truth_of = {r[0]: np.asarray(r[1], dtype=np.int32).reshape(S, T) for r in recv}
-    rng = np.random.default_rng([args.seed, 2000 + rank])
-    waves = []
+    # ---- per-epoch history pipeline.  Wave w of epoch e on this rank is chunk w of
+    # the HistoPipe group it serves; under the alternating group order the whole group (so the whole wave)
+    # moves to one rank at the next epoch, where it is that rank's wave w.  After each step the wave's
+    # finished rollouts stay in HBM: hs_pack_rows + all-to-all-v route them to their next owner, which turns
+    # them into the next epoch's history on a side stream (hs_mutate_bursts: G s-similar relatives per
+    # rollout -- the stand-in for policy drift, the (D) definition -- then K1) while the next wave rolls out.
+    # Weights are fixed, so a prompt's rollout in epoch e + 1 equals its epoch-e rollout: the routed tokens
+    # are also the bit-exactness reference of the step that uses them.
+    side_st = torch.cuda.Stream(dev)
+    stream = torch.cuda.current_stream(dev)
     resp_off = np.arange(B * G + 1, dtype=np.int64) * T
     slot_resp_off = np.arange(B + 1, dtype=np.int64) * G
-    for wv in range(n_waves):
-        pids = mine2[wv * per_wave:(wv + 1) * per_wave]
-        expect = np.concatenate([truth_of[p] for p in pids])            # [B, T]
-        hist, rew = derived_history(rng, expect, args.similarity, G, cfg.vocab, args.history)
-        waves.append({"pids": pids, "expect": expect, "keys": seq_keys(pids),
-                      "h_prompts": torch.from_numpy(sample_prompts(prompt_tokens, pids, S, cfg.vocab)).pin_memory(),
-                      "h_hist": torch.from_numpy(hist.reshape(-1)).pin_memory(),
-                      "reward_fx": (rew.reshape(-1) * float(1 << 32)).astype(np.int64)})
-    owner3 = W.owner_map(W.assign_prompts(medians, world, 3))
-    out_tok = torch.empty((B, T), dtype=torch.int32).pin_memory()
     slots = np.arange(B)                 # one history slot per sequence: its G previous-epoch relatives
-    stream = torch.cuda.current_stream(dev)
-    acc = {"ms": [], "res": [], "exact": True, "route_ms": [], "n": 0, "ingest_ms": []}
+    hist_rng = np.random.default_rng([args.seed, 2000 + rank])
+    acc = {"ms": [], "res": [], "exact": True, "route_ms": [], "n": 0, "ingest_ms": [], "epoch": 2}
+    lib_hs = _lib.load()
+
+    def ingest_routed(routed, epoch, wv_idx):
+        """On side_st: history of the next epoch's wave from its routed rollouts; returns the wave record."""
+        order = np.argsort(routed.keys, kind="stable")
+        assert (order == np.arange(len(order))).all(), "routed records arrive in sequence-key order"
+        assert len(routed.keys) == B and (np.diff(routed.resp_off) == T).all()
+        pids = [int(p) for p in routed.pids[::S]]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(side_st):
+            e0.record(side_st)
+            truth = routed.tokens.view(B, T)
+            if args.history == "D":
+                hist = torch.empty(B * G * T, dtype=torch.int32, device=dev)
+                rfx = torch.empty(B * G, dtype=torch.int64, device=dev)
+                d_off = torch.as_tensor(routed.resp_off).to(dev, non_blocking=True)
+                _lib.check(lib_hs.hs_mutate_bursts(truth.data_ptr(), d_off.data_ptr(), B, G, float(args.similarity),
+                                                   4.0, cfg.vocab, (args.seed << 20) ^ (epoch << 8) ^ wv_idx,
+                                                   hist.data_ptr(), rfx.data_ptr(), side_st.cuda_stream))
+                reward_fx = rfx.cpu().numpy()
+            else:   # (T) tracegen semantics: host restatement (synth.mutate), not pipelined
+                h, rew = derived_history(hist_rng, truth.cpu().numpy(), args.similarity, G, cfg.vocab, "T")
+                hist = torch.from_numpy(h.reshape(-1)).to(dev)
+                reward_fx = (rew.reshape(-1) * float(1 << 32)).astype(np.int64)
+            idx = GpuIndex.from_arrays(hist, resp_off, slot_resp_off, reward_fx, stream=side_st)   # K1
+            e1.record(side_st)
+            ready = torch.cuda.Event()
+            ready.record(side_st)
+        return {"pids": pids, "truth": truth, "keys": routed.keys.astype(np.int32), "index": idx, "ready": ready,
+                "ev": (e0, e1), "h_prompts": torch.from_numpy(sample_prompts(prompt_tokens, pids, S,
+                                                                             cfg.vocab)).pin_memory()}
+
+    def route(d_tokens, pids, epoch_next):
+        """Route a finished wave (device [B, T]) to the owners of its prompts at epoch_next (side_st)."""
+        owner = W.owner_map(W.assign_prompts(medians, world, epoch_next))
+        keys = seq_keys(pids)
+        seq_pid = np.repeat(np.asarray(pids, np.int64), S)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        side_st.wait_event(ev)
+        d_tokens.record_stream(side_st)
+        with torch.cuda.stream(side_st):
+            return W.route_rollouts_device(d_tokens, np.full(B, T, np.int64), seq_pid, keys,
+                                           np.full(B, 1 << 32, np.int64), owner, rank, world, stream=side_st)
+
+    # epoch 1 -> epoch 2: route the plain rollouts and build every wave's epoch-2 history
+    waves = []
+    for wv in range(n_waves):
+        pids = mine1[wv * per_wave:(wv + 1) * per_wave]
+        d_tok = torch.as_tensor(np.concatenate([outs[p] for p in pids])).to(dev)
+        waves.append(ingest_routed(route(d_tok, pids, 2), 2, wv))
+    torch.cuda.synchronize()
+    out_tok = torch.empty((B, T), dtype=torch.int32).pin_memory()
 
     def step():
-        wv = waves[acc["n"] % n_waves]
+        k = acc["n"]
         acc["n"] += 1
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        wi = k % n_waves
+        epoch = 2 + k // n_waves
+        wv = waves[wi]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d_prompts = wv["h_prompts"].to(dev, non_blocking=True)
-        d_hist = wv["h_hist"].to(dev, non_blocking=True)
         e0.record(stream)
-        idx = GpuIndex.from_arrays(d_hist, resp_off, slot_resp_off, wv["reward_fx"])   # K1: ingest the history
-        e2.record(stream)
-        res = eng.rollout(d_prompts, [T] * B, slots=slots, index=idx, speculate=True, seq_keys=wv["keys"])
+        stream.wait_event(wv["ready"])                 # the wave's history (built on side_st) is in place
+        res = eng.rollout(d_prompts, [T] * B, slots=slots, index=wv["index"], speculate=True,
+                          seq_keys=wv["keys"])
         e1.record(stream)
         out_tok.copy_(torch.from_numpy(res.tokens))   # results already read back by rollout(); keep pinned copy
-        e1.synchronize()
-        # per-epoch history update: this step's rollouts go to their next owners
+        acc["exact"] &= bool(torch.equal(res.d_tokens, wv["truth"]))
+        # per-epoch history update: route this wave to its next owner, whose next-epoch history of it builds
+        # on the side stream under the next wave's rollout
         t0 = time.perf_counter()
-        W.route_rollouts([(pid, res.tokens[i * S:(i + 1) * S].reshape(-1), 1.0) for i, pid in enumerate(wv["pids"])],
-                         owner3, rank, world, device=dev if world > 1 else "cpu")
+        routed = route(res.d_tokens, wv["pids"], epoch + 1)
         acc["route_ms"].append(1e3 * (time.perf_counter() - t0))
+        acc["ingest_ms"].append(wv["ev"])
+        waves[wi] = ingest_routed(routed, epoch + 1, wi)
+        e1.synchronize()
         acc["ms"].append(e0.elapsed_time(e1))
-        acc["ingest_ms"].append(e0.elapsed_time(e2))
         acc["res"].append(res)
-        acc["exact"] &= bool(np.array_equal(res.tokens, wv["expect"]))
 
     lc0, mc0, gl0 = _lib.load().hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
     e2e_ms, clocks = timed(step, args.steps, args.warmup, dist, stream, dist.local)
@@ -568,7 +615,8 @@ def run_rollout(args, dist, pk):
         "profiled_forward": {"seqs": B, "rows_per_seq_mean": q_mean, "rows_per_seq_max": int(q_lens.max()),
                              "ctx": P + T // 2, "M": M, "note": "verify-block sizes sampled from this run's histogram"},
         "verify_rows_hist": {str(i): int(c) for i, c in enumerate(qh) if c},
-        "step_ms": acc["ms"], "ingest_ms": acc["ingest_ms"], "nonspec_wave_ms": base_ms,
+        "step_ms": acc["ms"], "ingest_ms": [a.elapsed_time(b) for a, b in acc["ingest_ms"]],
+        "route_ms": acc["route_ms"], "nonspec_wave_ms": base_ms,
         "engine_iterations": [r.iterations for r in timed_res]})
     sampling = args.temperature > 0
     line = {
@@ -590,10 +638,11 @@ def run_rollout(args, dist, pk):
         "collectives": {"weight_broadcast_ms": bcast_ms, "rollout_route_ms_per_step": float(np.mean(
             acc["route_ms"][-args.steps:])), "note": "epoch-boundary only: NCCL broadcast of the policy, "
                                                      "all-to-all-v of finished rollouts to next-step owners"},
-        "ingest_ms_per_step": float(np.mean(acc["ingest_ms"][-args.steps:])),
+        "ingest_ms_per_step": float(np.mean([a.elapsed_time(b) for a, b in acc["ingest_ms"][-args.steps:]])),
         "distinct_4gram_ratio": distinct,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(waves[0]["h_prompts"].numel() * 4
-                                                                            + waves[0]["h_hist"].numel() * 4),
+                                                                            + (0 if args.history == "D" else
+                                                                               B * G * T * 4)),
                 "d2h_bytes_per_step": int(out_tok.numel() * 4 + B * 5 * 8)},
         "gpu_launches": int(launches),
         "roofline": roof,

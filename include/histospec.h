@@ -187,6 +187,39 @@ int hs_similarity_replay_isa(const HsIndexView* view, const int32_t* d_isa, int3
                              const int32_t* d_tokens, const int64_t* d_resp_off, const int32_t* d_slot_of_resp,
                              int32_t prefix_len, int64_t* d_accepted, hs_stream_t stream);
 
+/* Continuous batching (engine lanes): lane d_lane[i] takes a new sequence whose
+ * generated tokens so far are d_tok[d_tok_off[i] : d_tok_off[i+1]] (empty for a fresh prompt; a migrated
+ * rollout's prefix, whose KV the admission prefill recomputed) followed by d_argmax[d_first_row[i]] when
+ * d_first_row[i] >= 0.  Target length, history slot (-1: none), speculation flag, AIMD window, prefix
+ * length and stats [5] are set from the inputs (a fresh sequence: window_init, prefix_init, {1,0,0,0,1} --
+ * its iteration 0 is a plain decode); draft / lookup flags are cleared.  d_prompt_len / d_seq_key (the
+ * engine's per-lane prompt length and sampling key) are optional, in/out pairs together. */
+int hs_lane_admit(int32_t n, const int32_t* d_lane, const int32_t* d_tok, const int64_t* d_tok_off,
+                  const int32_t* d_argmax, const int32_t* d_first_row, const int32_t* d_target,
+                  const int32_t* d_slot, const uint8_t* d_spec, const int32_t* d_window, const int32_t* d_prefix,
+                  const int64_t* d_stats, const int32_t* d_prompt_len_in, const int32_t* d_key_in,
+                  int32_t* d_gen_tok, int32_t gen_stride, int32_t* d_gen_len, int32_t* d_target_len,
+                  int32_t* d_slots, uint8_t* d_speculate, int32_t* d_window_out, int32_t* d_prefix_out,
+                  int64_t* d_stats_out, int32_t* d_draft_len, uint8_t* d_looked, uint8_t* d_found,
+                  int32_t* d_prompt_len, int32_t* d_seq_key, hs_stream_t stream);
+
+/* ---- per-epoch history update (hs_route.cu, history.py:396-437, io.py:41-88) ----
+ *
+ * hs_pack_rows: d_dst[d_dst_off[i] + j] = d_src[d_row[i] * src_stride + j] for j < d_len[i] -- gathers the
+ * finished rollouts of a step (rows of the engine's [n_seq, stride] token matrix) into one flat buffer in
+ * routing order (the send buffer of the all-to-all-v that moves them to their next owners). */
+int hs_pack_rows(const int32_t* d_src, int64_t src_stride, const int32_t* d_row, const int64_t* d_len,
+                 const int64_t* d_dst_off, int32_t n, int32_t* d_dst, hs_stream_t stream);
+
+/* hs_mutate_bursts: for each routed rollout i (tokens d_src[d_src_off[i] : d_src_off[i+1]]) write G
+ * independent s-similar copies (tracegen's burst semantics, tracegen.py:78-120; counter-hash RNG keyed by
+ * (seed, i, g)) at d_dst + G * d_src_off[i] + g * len_i, and a Bernoulli(0.5) reward in fixed point to
+ * d_reward_fx[i * G + g].  The bench's stand-in for policy drift between epochs (SURVEY.md 8(d), (D)
+ * definition), feeding hs_index_build directly. */
+int hs_mutate_bursts(const int32_t* d_src, const int64_t* d_src_off, int32_t n, int32_t G, double s,
+                     double burst, int32_t vocab, uint64_t seed, int32_t* d_dst, int64_t* d_reward_fx,
+                     hs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 # library name -> sources
 LIBS = {
-    "libhistospec.so": ["hs_index.cu", "hs_draft.cu", "hs_accept.cu"],
+    "libhistospec.so": ["hs_index.cu", "hs_draft.cu", "hs_accept.cu", "hs_route.cu"],
     "libhsmodel.so": ["hm_ops.cu", "hm_gemm.cu", "hm_attn.cu", "hm_attn_tc.cu", "hm_fp32.cu"],
 }
 

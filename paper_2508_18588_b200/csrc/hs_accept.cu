@@ -334,6 +334,81 @@ extern "C" int hs_accept_greedy(int32_t n_seq, const int32_t* d_argmax, const in
   return HS_OK;
 }
 
+namespace hs {
+namespace acc {
+
+// Continuous batching: (re)initialise engine lanes for newly admitted sequences (one CTA per lane).
+// Lane state becomes that of a ResponseContext (spec_engine.py:174-187) holding tokens[off_i : off_i+1]
+// (a migrated rollout's generated prefix, or nothing) followed by argmax[first_row_i] when first_row_i >= 0
+// (the token the admission prefill produced), with the carried AIMD window, prefix length and stats.
+__global__ void k_lane_admit(int32_t n, const int32_t* __restrict__ lane, const int32_t* __restrict__ tok,
+                             const int64_t* __restrict__ tok_off, const int32_t* __restrict__ argmax,
+                             const int32_t* __restrict__ first_row, const int32_t* __restrict__ target,
+                             const int32_t* __restrict__ slot, const uint8_t* __restrict__ spec,
+                             const int32_t* __restrict__ window_in, const int32_t* __restrict__ prefix_in,
+                             const int64_t* __restrict__ stats_in, const int32_t* __restrict__ prompt_len_in,
+                             const int32_t* __restrict__ key_in, int32_t* __restrict__ gen_tok, int32_t gen_stride,
+                             int32_t* __restrict__ gen_len, int32_t* __restrict__ target_len,
+                             int32_t* __restrict__ slots, uint8_t* __restrict__ speculate,
+                             int32_t* __restrict__ window, int32_t* __restrict__ prefix_len,
+                             int64_t* __restrict__ stats, int32_t* __restrict__ draft_len,
+                             uint8_t* __restrict__ looked, uint8_t* __restrict__ found,
+                             int32_t* __restrict__ prompt_len, int32_t* __restrict__ seq_key) {
+  for (int32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int32_t l = lane[i];
+    const int64_t o = tok_off[i];
+    const int32_t g = (int32_t)(tok_off[i + 1] - o);
+    int32_t* row = gen_tok + (int64_t)l * gen_stride;
+    for (int32_t j = threadIdx.x; j < g; j += blockDim.x) row[j] = tok[o + j];
+    if (threadIdx.x == 0) {
+      const int32_t fr = first_row[i];
+      if (fr >= 0) row[g] = argmax[fr];
+      gen_len[l] = g + (fr >= 0 ? 1 : 0);
+      target_len[l] = target[i];
+      slots[l] = slot[i];
+      speculate[l] = spec[i];
+      window[l] = window_in[i];
+      prefix_len[l] = prefix_in[i];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) stats[5 * (int64_t)l + c] = stats_in[5 * (int64_t)i + c];
+      draft_len[l] = 0;
+      looked[l] = 0;
+      found[l] = 0;
+      if (prompt_len) prompt_len[l] = prompt_len_in[i];
+      if (seq_key) seq_key[l] = key_in[i];
+    }
+  }
+}
+
+}  // namespace acc
+}  // namespace hs
+
+extern "C" int hs_lane_admit(int32_t n, const int32_t* d_lane, const int32_t* d_tok, const int64_t* d_tok_off,
+                             const int32_t* d_argmax, const int32_t* d_first_row, const int32_t* d_target,
+                             const int32_t* d_slot, const uint8_t* d_spec, const int32_t* d_window,
+                             const int32_t* d_prefix, const int64_t* d_stats, const int32_t* d_prompt_len_in,
+                             const int32_t* d_key_in, int32_t* d_gen_tok, int32_t gen_stride, int32_t* d_gen_len,
+                             int32_t* d_target_len, int32_t* d_slots, uint8_t* d_speculate, int32_t* d_window_out,
+                             int32_t* d_prefix_out, int64_t* d_stats_out, int32_t* d_draft_len, uint8_t* d_looked,
+                             uint8_t* d_found, int32_t* d_prompt_len, int32_t* d_seq_key, hs_stream_t stream) {
+  if (n < 0 || gen_stride < 1) {
+    hs_set_error("hs_lane_admit: n >= 0 and gen_stride >= 1 required");
+    return HS_ERR_INVALID;
+  }
+  if ((d_prompt_len == nullptr) != (d_prompt_len_in == nullptr) || (d_seq_key == nullptr) != (d_key_in == nullptr)) {
+    hs_set_error("hs_lane_admit: per-lane prompt_len / seq_key inputs and outputs go together");
+    return HS_ERR_INVALID;
+  }
+  if (n == 0) return HS_OK;
+  hs_count_launches(1);
+  acc::k_lane_admit<<<n < 1024 ? n : 1024, 128, 0, (cudaStream_t)stream>>>(
+      n, d_lane, d_tok, d_tok_off, d_argmax, d_first_row, d_target, d_slot, d_spec, d_window, d_prefix, d_stats,
+      d_prompt_len_in, d_key_in, d_gen_tok, gen_stride, d_gen_len, d_target_len, d_slots, d_speculate, d_window_out,
+      d_prefix_out, d_stats_out, d_draft_len, d_looked, d_found, d_prompt_len, d_seq_key);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
 extern "C" int hs_replay_fused(const HsIndexView* view, int32_t n_seq, const int32_t* d_slot_of_seq,
                                const int32_t* d_truth, const int64_t* d_truth_off, const uint8_t* d_speculate,
                                int32_t* d_tpi, int32_t* d_n_iter, int64_t* d_stats, HsSpecConfig cfg,

@@ -111,6 +111,230 @@ class RolloutEngine:
         state.accept_greedy(first, q_off)
         return rows
 
+    # -------------------------------------------------------------- continuous batching
+    def _prefill_rows(self, reqs, lanes, seq_keys):
+        """Admission prefill: KV of every request's context (prompt + generated[:-1]) into its lane's slot, in
+        forwards of <= prefill_rows rows whose entries are chunks of <= `chunk` rows (one attention entry
+        per chunk, positions continuing the sequence).  Returns (first-token argmax per request, -1 for
+        migrated ones; device int32 [n]), rows."""
+        import torch
+        dev = self.device
+        chunk = 2048
+        ent = []   # (request i, start, length)
+        ctx = []
+        for i, r in enumerate(reqs):
+            g = 0 if r.generated is None else len(r.generated)
+            c = np.asarray(r.prompt, np.int32) if g == 0 else np.concatenate(
+                [np.asarray(r.prompt, np.int32), np.asarray(r.generated[:g - 1], np.int32)])
+            ctx.append(c)
+            for a in range(0, len(c), chunk):
+                ent.append((i, a, min(chunk, len(c) - a)))
+        first = torch.full((len(reqs),), -1, dtype=torch.int32, device=dev)
+        rows = 0
+        e = 0
+        while e < len(ent):
+            batch, m = [], 0
+            while e < len(ent) and (not batch or m + ent[e][2] <= self.prefill_rows):
+                batch.append(ent[e])
+                m += ent[e][2]
+                e += 1
+            toks = np.concatenate([ctx[i][a:a + n] for i, a, n in batch]).astype(np.int32)
+            pos = np.concatenate([np.arange(a, a + n, dtype=np.int32) for i, a, n in batch])
+            rslot = np.concatenate([np.full(n, lanes[i], np.int32) for i, a, n in batch])
+            rkey = np.concatenate([np.full(n, seq_keys[i], np.int32) for i, a, n in batch])
+            qlen = np.array([n for _, _, n in batch], np.int32)
+            qoff = np.concatenate([[0], np.cumsum(qlen)[:-1]]).astype(np.int32)
+            pos0 = np.array([a for _, a, _ in batch], np.int32)
+            kvs = np.array([lanes[i] for i, _, _ in batch], np.int32)
+            nb = len(batch)
+            self.tokens[:m] = torch.from_numpy(toks).to(dev, non_blocking=True)
+            self.pos[:m] = torch.from_numpy(pos).to(dev, non_blocking=True)
+            self.row_slot[:m] = torch.from_numpy(rslot).to(dev, non_blocking=True)
+            self.row_key[:m] = torch.from_numpy(rkey).to(dev, non_blocking=True)
+            q_off = torch.from_numpy(qoff).to(dev, non_blocking=True)
+            q_len = torch.from_numpy(qlen).to(dev, non_blocking=True)
+            p0 = torch.from_numpy(pos0).to(dev, non_blocking=True)
+            kv = torch.from_numpy(kvs).to(dev, non_blocking=True)
+            am = self.fwd.run(m, self.tokens, self.pos, self.row_slot, q_off, q_len, p0, kv, nb, int(qlen.max()),
+                              row_key=self.row_key)
+            # fresh requests whose context ends in this forward: their first response token
+            last = {}
+            for j, (i, a, n) in enumerate(batch):
+                if reqs[i].generated is None and a + n == len(ctx[i]):
+                    last[i] = int(qoff[j]) + n - 1
+            if last:
+                idx = torch.as_tensor(list(last.values()), dtype=torch.long).to(dev, non_blocking=True)
+                dst = torch.as_tensor(list(last.keys()), dtype=torch.long).to(dev, non_blocking=True)
+                first.index_copy_(0, dst, am.index_select(0, idx))
+            rows += m
+        return first, rows
+
+    def rollout_stream(self, requests, index=None, speculate=True, admit_min=None, on_check=None):
+        """Continuous batching: every engine lane runs a sequence; finished lanes are refilled from the
+        request queue (in the given order -- the caller puts the predicted-longest first) by an admission
+        prefill between CUDA-graph replays, so a long tail does not idle the batch.
+
+        on_check(busy: {lane: key}, gen_len: np.ndarray, iteration) -> lanes to evict, called every
+        `check_every` iterations: their state leaves as SeqRequest (migration with KV recompute).
+        """
+        import collections
+        import torch
+        from .spec_engine import SpecBatch
+        if self.attention is not None:
+            from .model import set_attention_family
+            set_attention_family(self.attention)
+        reqs = list(requests)
+        n = self.n_slots
+        dev = self.device
+        cfgs = self.spec
+        max_t = max([int(r.target_len) for r in reqs] + [1])
+        max_ctx = max([len(r.prompt) + int(r.target_len) for r in reqs] + [1])
+        if max_ctx > self.max_len:
+            raise ValueError("prompt + target exceeds max_len")
+        spec_on = bool(speculate and index is not None and cfgs.enabled)
+        state = SpecBatch(np.full(n, -1, np.int32), np.zeros(n, np.int32), cfgs, speculate=np.zeros(n, np.uint8),
+                          device=dev, max_len=max_t, record_tpi=False)
+        i32 = dict(dtype=torch.int32, device=dev)
+        prompt_len = torch.zeros(n, **i32)
+        seq_key = torch.zeros(n, **i32)
+        acc = torch.zeros(4, dtype=torch.int64, device=dev)
+        qhist = torch.zeros(self.max_q + 1, dtype=torch.int64, device=dev)
+        q_cap = self.max_q if spec_on else 1
+        R = min(self.fwd.max_rows, n * q_cap)
+        L = lib()
+        st = torch.cuda.current_stream(dev)
+
+        def iteration():
+            s = torch.cuda.current_stream(dev)
+            if spec_on:
+                state.propose(index, s)
+            check(L.hm_build_verify_batch(
+                n, state.gen_tok.data_ptr(), state.gen_stride, state.gen_len.data_ptr(), state.target_len.data_ptr(),
+                prompt_len.data_ptr(), state.draft_tok.data_ptr(), state.draft_tok.shape[1],
+                state.draft_len.data_ptr(), self.kv_slot.data_ptr(), self.tokens.data_ptr(), self.pos.data_ptr(),
+                self.row_slot.data_ptr(), self.q_off.data_ptr(), self.q_len.data_ptr(), self.pos0.data_ptr(),
+                self.d_m.data_ptr(), acc.data_ptr(), qhist.data_ptr(), qhist.numel(), seq_key.data_ptr(),
+                self.row_key.data_ptr(), s.cuda_stream))
+            am = self.fwd.run(R, self.tokens, self.pos, self.row_slot, self.q_off, self.q_len, self.pos0,
+                              self.kv_slot, n, q_cap, stream=s, m_dev=self.d_m, row_key=self.row_key)
+            state.accept_greedy(am, self.q_off, s)
+
+        lib_hs = _lib.load()
+        admit_min = max(1, n // 32) if admit_min is None else int(admit_min)
+        queue = collections.deque(reqs)
+        busy = {}                      # lane -> request
+        free = list(range(n))[::-1]
+        out_tok, out_stats, evicted = {}, {}, []
+        prefill_rows = admissions = 0
+        busy_iters = 0
+        graph = None
+        per_iter = 0
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(st)
+        it_host = 0
+
+        def admit(batch_reqs):
+            nonlocal prefill_rows, admissions
+            lanes = [free.pop() for _ in batch_reqs]
+            keys = [int(r.key) for r in batch_reqs]
+            first, rows = self._prefill_rows(batch_reqs, lanes, keys)
+            prefill_rows += rows
+            admissions += len(batch_reqs)
+            gen = [np.zeros(0, np.int32) if r.generated is None else np.asarray(r.generated, np.int32)
+                   for r in batch_reqs]
+            off = np.concatenate([[0], np.cumsum([len(g) for g in gen])]).astype(np.int64)
+            fresh = np.array([r.generated is None for r in batch_reqs])
+            stats = np.stack([np.array([1, 0, 0, 0, 1], np.int64) if r.stats is None else
+                              np.asarray(r.stats, np.int64) for r in batch_reqs])
+            win = np.array([cfgs.window_init if r.window is None else r.window for r in batch_reqs], np.int32)
+            pre = np.array([cfgs.prefix_init if r.prefix_len is None else r.prefix_len for r in batch_reqs], np.int32)
+            spec = np.array([int(spec_on and r.slot >= 0) for r in batch_reqs], np.uint8)
+            h = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)  # noqa: E731
+            d = dict(lane=h(np.array(lanes, np.int32)), tok=h(np.concatenate(gen + [np.zeros(1, np.int32)])),
+                     off=h(off), first_row=h(np.where(fresh, np.arange(len(lanes)), -1).astype(np.int32)),
+                     target=h(np.array([r.target_len for r in batch_reqs], np.int32)),
+                     slot=h(np.array([r.slot for r in batch_reqs], np.int32)), spec=h(spec), win=h(win), pre=h(pre),
+                     stats=h(stats), plen=h(np.array([len(r.prompt) for r in batch_reqs], np.int32)),
+                     key=h(np.array(keys, np.int32)))
+            _lib.check(lib_hs.hs_lane_admit(
+                len(lanes), d["lane"].data_ptr(), d["tok"].data_ptr(), d["off"].data_ptr(), first.data_ptr(),
+                d["first_row"].data_ptr(), d["target"].data_ptr(), d["slot"].data_ptr(), d["spec"].data_ptr(),
+                d["win"].data_ptr(), d["pre"].data_ptr(), d["stats"].data_ptr(), d["plen"].data_ptr(),
+                d["key"].data_ptr(), state.gen_tok.data_ptr(), state.gen_stride, state.gen_len.data_ptr(),
+                state.target_len.data_ptr(), state.slots.data_ptr(), state.speculate.data_ptr(),
+                state.window.data_ptr(), state.prefix_len.data_ptr(), state.stats.data_ptr(),
+                state.draft_len.data_ptr(), state.looked.data_ptr(), state.found.data_ptr(), prompt_len.data_ptr(),
+                seq_key.data_ptr(), st.cuda_stream))
+            for ln, r in zip(lanes, batch_reqs):
+                busy[ln] = r
+
+        def harvest(lanes, to_out=True):
+            if not lanes:
+                return
+            li = torch.as_tensor(lanes, dtype=torch.long).to(dev)
+            toks = state.gen_tok.index_select(0, li).cpu().numpy()
+            sts = state.stats.index_select(0, li).cpu().numpy()
+            if not to_out:
+                win = state.window.index_select(0, li).cpu().numpy()
+                pre = state.prefix_len.index_select(0, li).cpu().numpy()
+                gl = state.gen_len.index_select(0, li).cpu().numpy()
+                state.target_len.index_fill_(0, li, 0)     # the lane stops decoding
+            for j, ln in enumerate(lanes):
+                r = busy.pop(ln)
+                if to_out:
+                    out_tok[r.key] = toks[j, :r.target_len].copy()
+                    out_stats[r.key] = sts[j].copy()
+                else:
+                    evicted.append(SeqRequest(r.key, r.prompt, r.target_len, r.slot, toks[j, :gl[j]].copy(),
+                                              int(win[j]), int(pre[j]), sts[j].copy()))
+                free.append(ln)
+
+        while queue or busy:
+            if queue and free and (len(free) >= admit_min or not busy or len(queue) <= len(free)):
+                k = min(len(free), len(queue))
+                admit([queue.popleft() for _ in range(k)])
+            if graph is None and self.use_graphs:
+                iteration()            # eager first iteration (kernel attributes), then capture
+                it_host += 1
+                busy_iters += len(busy)
+                graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(st)
+                c0 = launch_count()
+                with torch.cuda.graph(graph, stream=side):
+                    iteration()
+                per_iter = launch_count() - c0
+                self.graph_launches -= per_iter
+                st.wait_stream(side)
+            for _ in range(self.check_every):
+                if self.use_graphs:
+                    graph.replay()
+                    self.graph_launches += per_iter
+                else:
+                    iteration()
+            it_host += self.check_every
+            busy_iters += self.check_every * len(busy)
+            gl = state.gen_len.cpu().numpy()
+            tl = state.target_len.cpu().numpy()
+            done = [ln for ln in busy if gl[ln] >= tl[ln]]
+            harvest(done)
+            if on_check is not None and busy:
+                ev = list(on_check({ln: busy[ln].key for ln in busy}, gl, it_host) or [])
+                harvest([ln for ln in ev if ln in busy], to_out=False)
+        ev1.record(st)
+        torch.cuda.synchronize(dev)
+        a = acc.cpu().numpy()
+        cfg = self.cfg
+        rows = int(a[0])
+        flops = 2.0 * (cfg.body_params() + cfg.vocab * cfg.d_model) * (rows + prefill_rows) \
+            + 4.0 * cfg.n_layers * cfg.n_heads * cfg.head_dim * float(a[2])
+        qh = qhist.cpu().numpy()
+        qh[0] = 0
+        res = StreamResult(out_tok, out_stats, evicted, int(a[1]), ev0.elapsed_time(ev1), rows, prefill_rows,
+                           admissions, flops, float(cfg.kv_bytes_per_token) * float(a[3]), qh, busy_iters)
+        res.weight_bytes = float(self.w.nbytes())
+        return res
+
     def rollout(self, prompts, target_len, slots=None, index=None, speculate=True, record_tpi=False,
                 recent_acceptance=None, seq_keys=None):
         """Generate target_len[b] tokens for each prompt row b (greedy), drafting from `index`.
@@ -210,12 +434,51 @@ class RolloutEngine:
         qh[0] = 0   # finished sequences
         res = RolloutResult(tokens=gen, stats=stats, iterations=iters, rows=rows, gpu_ms=gpu_ms, flops=flops,
                             kv_bytes=kv_bytes, qlen_hist=qh)
+        res.d_tokens = state.gen_tok[:, :int(tl.max())]   # device copy (epoch pipeline: routed without a host trip)
         per = max(1, self.prefill_rows // P)
         res.forwards = (iters - 1) + (B + per - 1) // per   # decode/verify forwards + prefill chunks
         res.weight_bytes = float(self.w.nbytes())
         if record_tpi:
             res.tokens_per_iter = state.tokens_per_iter()
         return res
+
+
+@dataclass
+class SeqRequest:
+    """One sequence for the continuous-batching engine (RolloutEngine.rollout_stream).
+
+    A fresh rollout has `generated` None.  A migrated one (sim.py:719-779) carries the
+    tokens it generated so far plus its HistoSpec state (AIMD window, prefix length, SpecStats): admission
+    recomputes the KV of prompt + generated[:-1] by prefill and the rollout continues where it stopped.
+    """
+    key: int                      # global sequence key: sampling key and result id
+    prompt: np.ndarray            # int32 prompt tokens
+    target_len: int               # response length to generate
+    slot: int = -1                # history slot in the index (-1: no history)
+    generated: np.ndarray | None = None
+    window: int | None = None
+    prefix_len: int | None = None
+    stats: np.ndarray | None = None
+
+
+@dataclass
+class StreamResult:
+    tokens: dict                  # key -> int32 response tokens
+    stats: dict                   # key -> int64 [5] SpecStats
+    evicted: list                 # SeqRequest of sequences handed out by `on_check` (migration)
+    iterations: int
+    gpu_ms: float
+    rows: int                     # verify / decode rows
+    prefill_rows: int
+    admissions: int
+    flops: float = 0.0
+    kv_bytes: float = 0.0
+    qlen_hist: np.ndarray = None
+    busy_lane_iters: int = 0      # sum over iterations of busy lanes (occupancy = / (iterations * lanes))
+
+    @property
+    def generated(self) -> int:
+        return int(sum(int(v[0]) for v in self.stats.values()))
 
 
 def profile_forward(engine: RolloutEngine, B: int, ctx: int, q, launch_rows=None, launch_q=None):

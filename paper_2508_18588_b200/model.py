@@ -189,9 +189,41 @@ class Weights:
                 layer["gate"], layer["up"] = gate, up
             self.layers.append(layer)
         self.final_ln = torch.ones(d, dtype=torch.bfloat16, device=device)
+        self._flatten()
         half = hd // 2
         inv = 1.0 / (cfg.rope_theta ** (np.arange(half, dtype=np.float64) * 2.0 / hd))
         self._inv_freq = inv
+
+    def tensors(self):
+        """Every weight tensor, in a fixed order (the tied LM head once)."""
+        out = [self.embed] + ([] if self.cfg.tied else [self.lm_head]) + [self.final_ln]
+        for layer in self.layers:
+            out += [layer[k] for k in ("ln1", "wqkv", "bqkv", "wo", "ln2", "wgu", "wd")]
+        return out
+
+    def _flatten(self):
+        """Re-home every weight in one contiguous bf16 buffer (`self.flat`), each tensor a 256-byte-aligned view,
+        so the epoch-boundary policy broadcast is one NCCL call (workers.broadcast_weights)."""
+        import torch
+        ts = self.tensors()
+        offs, n = [], 0
+        for t in ts:
+            offs.append(n)
+            n += (t.numel() + 127) // 128 * 128
+        flat = torch.empty(n, dtype=torch.bfloat16, device=ts[0].device)
+        views = []
+        for t, o in zip(ts, offs):
+            v = flat[o:o + t.numel()].view(t.shape)
+            v.copy_(t)
+            views.append(v)
+        it = iter(views)
+        self.embed = next(it)
+        self.lm_head = self.embed if self.cfg.tied else next(it)
+        self.final_ln = next(it)
+        for layer in self.layers:
+            for k in ("ln1", "wqkv", "bqkv", "wo", "ln2", "wgu", "wd"):
+                layer[k] = next(it)
+        self.flat = flat
 
     def rope_tables(self, max_pos, device):
         """cos/sin [max_pos, hd/2] fp32, computed in float64 on the host (same table for every backend)."""

@@ -61,3 +61,40 @@ def test_route_rollouts_all_to_all_world2():
         expect = [r for src in range(world) for r in out[src][0] if owner[r[0]] == rank]
         assert out[rank][1] == expect
     assert sum(len(out[k][1]) for k in range(world)) == len(sent)
+
+
+def _meta_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(10 + rank)
+    med = {i: float(100 + (i * 37) % 11) for i in range(12)}
+    mine = W.assign_prompts(med, world, 1)[rank]
+    pids = np.repeat(np.asarray(mine, np.int64), 2)
+    lens = rng.integers(1, 50, size=len(pids))
+    keys = np.arange(len(pids)) + 100 * rank
+    rew = rng.integers(0, 4, size=len(pids)) << 30
+    owner = W.owner_map(W.assign_prompts(med, world, 2))
+    plan = W.plan_routes(pids, lens, owner, world)
+    meta = np.stack([pids, keys, lens, rew], axis=1).astype(np.int64)
+    rc, got = W.exchange_route_meta(plan, meta, "cpu")
+    out[rank] = (meta.tolist(), got.tolist(), rc.tolist(), owner)
+    dist.destroy_process_group()
+
+
+def test_route_meta_exchange_world2():
+    """Device routing's host plan + record-table exchange (workers.plan_routes / exchange_route_meta)."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_meta_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    owner = out[0][3]
+    for rank in range(world):
+        expect = []
+        for src in range(world):
+            rows = [r for r in out[src][0] if owner[r[0]] == rank]
+            rows.sort(key=lambda r: r[0])            # send order: destination, prompt, input order (stable)
+            expect += rows
+        assert out[rank][1] == expect
+        assert [c[1] for c in out[rank][2]] == [sum(r[2] for r in out[src][0] if owner[r[0]] == rank)
+                                                for src in range(world)]
