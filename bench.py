@@ -664,6 +664,198 @@ def run_rollout(args, dist, pk):
     return line, {"cfg": cfg, "prompts": waves[0]["h_prompts"].numpy(), "T": T, "w": w}
 
 
+# ------------------------------------------------------------------ long-tail workload (configs[3])
+
+def tau_profile(eng, cfg, world, lanes, group_seqs, pk, dist):
+    """HistoPipe tau(len, k) from this engine's measured verify-forward times (rank 0, broadcast): a group of
+    `group_seqs` sequences of length len on k GPUs runs min(lanes, group_seqs / k) lanes per GPU for about
+    len / tokens-per-iteration iterations at mean context len / 2.  Returns workers.TauProfile."""
+    import torch
+    from paper_2508_18588_b200 import workers as W
+    from paper_2508_18588_b200.engine import profile_forward
+    lens = [512, 2048, 8192, 16384]
+    ks = list(range(1, world + 1))
+    grid = torch.zeros(len(lens), len(ks), dtype=torch.float64, device=eng.device)
+    if dist.rank == 0:
+        tpi = 3.0   # tokens per iteration assumed by the profile; TauProfile.accepted_per_pass rescales
+        for i, l in enumerate(lens):
+            for j, k in enumerate(ks):
+                b = max(1, min(lanes, -(-group_seqs // k)))
+                prof, _m = profile_forward(eng, b, min(eng.max_len - 40, 256 + l // 2), 4)
+                t_fwd = sum(v[0] for v in prof.values()) / 1e3
+                waves = -(-group_seqs // (b * k))
+                grid[i, j] = waves * (l / tpi) * t_fwd
+    if dist.pg is not None:
+        dist.pg.broadcast(grid, src=0)
+    g = grid.cpu().numpy()
+    return W.TauProfile.from_rows([(l, k, float(g[i, j])) for i, l in enumerate(lens) for j, k in enumerate(ks)])
+
+
+def run_longtail(args, dist, pk):
+    """configs[3]: long-tail response lengths (log-normal, clipped to [512, 16384]) on the continuous-batching
+    engine, prompts placed by HistoPipe (ranked groups, tau-profiled two-tier allocation, alternating order),
+    (D) histories at each similarity of the sweep.  One step = one speculative epoch of this rank's share."""
+    import torch
+    from paper_2508_18588_b200 import _lib
+    from paper_2508_18588_b200 import workers as W
+    from paper_2508_18588_b200.engine import RolloutEngine, SeqRequest
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import PRESETS, Weights
+    from paper_2508_18588_b200.model import lib as mlib
+
+    cfg = PRESETS[args.model]
+    dev = torch.device("cuda", dist.local)
+    torch.cuda.set_device(dev)
+    world, rank = dist.world, dist.rank
+    S, P, G = args.samples, args.prompt_len, 8
+    lo, hi = 512, 16384
+    lanes = args.batch
+    n_prompts = args.prompts * world                       # weak scaling: args.prompts per GPU
+    rng = np.random.default_rng([args.seed, 4242])
+    z = rng.standard_normal(n_prompts)
+    med = np.clip(np.exp(np.log(args.len_median) + args.len_sigma * z), lo, hi)
+    tgt = np.clip(np.rint(med[:, None] * np.exp(0.08 * rng.standard_normal((n_prompts, S)))), lo, hi).astype(int)
+    w = Weights(cfg, dev, seed=args.seed)
+
+    def make_engine(max_target):
+        # length-aware lanes: the slot-contiguous KV cache holds as many lanes as fit at this rank's longest
+        # assigned rollout (a rank serving a short HistoPipe group runs a wider batch)
+        ml = P + int(max_target) + 8
+        n = int(min(args.batch, max(8, args.kv_gb * 1e9 // ((ml + 34) * cfg.kv_bytes_per_token))))
+        return RolloutEngine(cfg, w, n_slots=n, max_len=ml, device=dev, attention=args.attention, check_every=8)
+
+    plan = None
+    if world > 1:
+        n_groups = max(2, world // 2)
+        groups = W.build_groups({p: float(med[p]) for p in range(n_prompts)}, n_groups)
+        probe = make_engine(hi)
+        tau = tau_profile(probe, cfg, world, probe.n_slots, len(groups[0].prompt_ids) * S, pk, dist)
+        del probe
+        torch.cuda.empty_cache()
+        lens_g = [g.representative_len for g in groups]
+        plan = (W.plan_makespan(lens_g, world, tau) if args.histopipe == "makespan"
+                else W.plan_allocation(lens_g, world, 0.0, tau, precision=0.01))
+        per_group = plan.per_group_workers if plan.feasible else W.partition_sizes(world, n_groups)
+        mine = W.assign_with_plan(groups, per_group, 1)[rank]
+    else:
+        mine = list(range(n_prompts))
+    eng = make_engine(tgt[mine].max())
+    lanes = eng.n_slots
+
+    def prompt_tokens(pid):
+        return np.random.default_rng([args.seed, 1000 + pid]).integers(0, cfg.vocab, size=P, dtype=np.int32)
+
+    prompts = sample_prompts(prompt_tokens, mine, S, cfg.vocab)
+    keys = [pid * S + j for pid in mine for j in range(S)]
+    targets = [int(tgt[pid, j]) for pid in mine for j in range(S)]
+    reqs = [SeqRequest(key=k, prompt=prompts[i], target_len=t, slot=i) for i, (k, t) in enumerate(zip(keys, targets))]
+    # length-aware admission: longest predicted (the prompt's last-epoch median) first
+    order = sorted(range(len(reqs)), key=lambda i: (-med[mine[i // S]], i))
+    queue = [reqs[i] for i in order]
+    # epoch 1: plain rollouts (the speculation-off baseline and the truth the speculative epochs reproduce)
+    base = eng.rollout_stream(queue, speculate=False)
+    n_tok = int(sum(targets))
+    truth = np.concatenate([base.tokens[k] for k in keys]).astype(np.int32)
+    resp_off = np.concatenate([[0], np.cumsum(targets)]).astype(np.int64)
+    d_truth = torch.from_numpy(truth).to(dev)
+    d_off = torch.from_numpy(resp_off).to(dev)
+    h_resp_off = np.concatenate([[0], np.cumsum(np.repeat(targets, G))]).astype(np.int64)
+    slot_resp_off = np.arange(len(reqs) + 1, dtype=np.int64) * G
+    lib_hs = _lib.load()
+    sweep = [float(x) for x in args.similarity_sweep.split(",")] if args.similarity_sweep else [args.similarity]
+    stream = torch.cuda.current_stream(dev)
+    rows = []
+    head = None
+    for si, sim in enumerate(sweep):
+        # (D) history of every sequence from its own epoch-1 output, on the device
+        hist = torch.empty(G * n_tok, dtype=torch.int32, device=dev)
+        rfx = torch.empty(G * len(reqs), dtype=torch.int64, device=dev)
+        _lib.check(lib_hs.hs_mutate_bursts(d_truth.data_ptr(), d_off.data_ptr(), len(reqs), G, sim, 4.0, cfg.vocab,
+                                           args.seed * 7919 + si, hist.data_ptr(), rfx.data_ptr(), stream.cuda_stream))
+        # hs_mutate_bursts lays member g of sequence i at G * off[i] + g * len[i]: slot-major, as K1 wants
+        idx = GpuIndex.from_arrays(hist, h_resp_off, slot_resp_off, rfx.cpu().numpy())
+        box = {}
+
+        def step():
+            box["res"] = eng.rollout_stream(queue, index=idx, speculate=True)
+
+        lc0, mc0, gl0 = lib_hs.hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
+        e2e_ms, clocks = timed(step, args.steps, args.warmup if si == 0 else 1, dist, stream, dist.local)
+        launches = ((lib_hs.hs_launch_count() - lc0) + (mlib().hm_launch_count() - mc0)
+                    + (eng.graph_launches - gl0)) // (args.steps + (args.warmup if si == 0 else 1))
+        res = box["res"]
+        exact = all(np.array_equal(res.tokens[k], base.tokens[k]) for k in keys)
+        st = np.sum([res.stats[k] for k in keys], axis=0)
+        value = dist.sum(n_tok) / (dist.max(e2e_ms) / 1e3)
+        row = {"similarity": sim, "value": value, "ms_per_step": e2e_ms,
+               "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
+               "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
+               "occupancy": res.busy_lane_iters / max(1, res.iterations * lanes),
+               "bit_exact_vs_greedy": bool(dist.sum(float(exact)) == world),
+               "speedup_vs_nonspec": value / (dist.sum(n_tok) / dist.max(base.gpu_ms / 1e3))}
+        rows.append(row)
+        if head is None:
+            head = (row, clocks, launches, res)
+    # static waves on the same workload (no refill: a wave lasts as long as its longest rollout)
+    waves_ms = 0.0
+    if args.compare_waves:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for a in range(0, len(queue), lanes):
+            chunk = queue[a:a + lanes]
+            r = eng.rollout(np.stack([q.prompt for q in chunk]), [q.target_len for q in chunk],
+                            slots=[q.slot for q in chunk], index=idx, speculate=True,
+                            seq_keys=[q.key for q in chunk])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        waves_ms = e0.elapsed_time(e1)
+    row, clocks, launches, res = head
+    nonspec = dist.sum(n_tok) / dist.max(base.gpu_ms / 1e3)
+    mine_stat = torch.tensor([float(n_tok), float(row["ms_per_step"]), float(lanes), float(row["occupancy"]),
+                              float(len(reqs)), float(max(targets))], dtype=torch.float64, device=dev)
+    if dist.pg is not None:
+        allst = [torch.zeros_like(mine_stat) for _ in range(world)]
+        dist.pg.all_gather(allst, mine_stat)
+    else:
+        allst = [mine_stat]
+    ranks = [dict(zip(("tokens", "step_ms", "lanes", "occupancy", "sequences", "longest"), t.cpu().tolist()))
+             for t in allst]
+    line = {
+        "metric": "rollout tokens/sec (greedy HistoSpec, long-tail lengths, continuous batching)",
+        "value": row["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": row["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic prompts (sample-id token per sample), random-init weights (seed %d), (D) history per "
+                "sequence (device burst mutation, G=%d)" % (args.seed, G),
+        "config": {"workload": "configs[3]: %s, %d prompts x %d samples per GPU, lengths log-normal median %d "
+                               "sigma %.2f clipped to [%d, %d] (%d tokens on rank 0), %d engine lanes" % (
+                                   cfg.name, args.prompts, S, args.len_median, args.len_sigma, lo, hi, n_tok, lanes),
+                   "lanes_per_rank": "KV budget %.0f GB / (longest assigned rollout x KV bytes per token), <= "
+                                     "--batch %d" % (args.kv_gb, args.batch),
+                   "step": "one speculative epoch of the rank's sequences through rollout_stream (admission "
+                           "prefill + CUDA-graph iterations; value includes prefill)",
+                   "parallelism": "dp%d, HistoPipe %s" % (world, "%s plan %s (d=%.3g s, t0=%.3g s)" % (
+                       args.histopipe, plan.per_group_workers, plan.gradient_d, plan.t0)
+                       if plan is not None and plan.feasible
+                       else "single rank" if plan is None else "infeasible plan -> equal split"),
+                   "l2": "KV cache (%.0f GB) streams far beyond the 126 MB L2" % (eng.cache.buf.numel() * 2 / 1e9)},
+        "e2e": {"value": row["value"], "unit": "tokens/s", "h2d_bytes_per_step": int(len(reqs) * P * 4),
+                "d2h_bytes_per_step": int(n_tok * 4 + len(reqs) * 40)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "sweep": rows,
+        "ranks": ranks,
+        "static_waves_value": (dist.sum(n_tok) / dist.max(waves_ms / 1e3)) if waves_ms else None,
+        "occupancy": row["occupancy"],
+        "nonspec_value": nonspec,
+        "tokens_per_iteration": row["tokens_per_iteration"],
+        "mean_accepted_per_verify": row["mean_accepted_per_verify"],
+        "bit_exact_vs_greedy": row["bit_exact_vs_greedy"],
+        "speedup_vs_nonspec": row["speedup_vs_nonspec"],
+    }
+    return line, {"cfg": cfg}
+
+
 # ------------------------------------------------------------------ lookup microbenchmark
 
 def run_lookup(args, dist, pk):
@@ -831,7 +1023,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup", "similarity"])
+    ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup", "similarity",
+                                                                  "longtail"])
     ap.add_argument("--model", default="qwen2.5-1.5b-shape")
     ap.add_argument("--batch", type=int, default=1024, help="resident sequences per wave (rollout)")
     ap.add_argument("--prompt-len", type=int, default=256)
@@ -847,6 +1040,13 @@ def main():
     ap.add_argument("--waves", type=int, default=4, help="rollout: waves of --batch sequences per GPU (cycled)")
     ap.add_argument("--history", default="D", choices=["D", "T"], help="similarity definition (SURVEY 8(d))")
     ap.add_argument("--temperature", type=float, default=0.0, help="0: greedy verify; > 0: rejection sampling")
+    ap.add_argument("--len-median", type=int, default=2048, help="longtail: median response length")
+    ap.add_argument("--len-sigma", type=float, default=0.8, help="longtail: log-normal sigma of lengths")
+    ap.add_argument("--similarity-sweep", default="", help="longtail: comma-separated similarities")
+    ap.add_argument("--compare-waves", action="store_true", help="longtail: also time static waves")
+    ap.add_argument("--kv-gb", type=float, default=120.0, help="longtail: KV-cache budget per GPU (GB)")
+    ap.add_argument("--histopipe", default="makespan", choices=["makespan", "gradient"],
+                    help="longtail: per-group GPU plan (gradient = the reference's plan_allocation)")
     ap.add_argument("--attention", default="tcgen05", choices=["tcgen05", "mma_sync"],
                     help="attention kernel family of the HistoSpec run (the baseline is measured with both)")
     args = ap.parse_args()
@@ -871,6 +1071,8 @@ def main():
         line, data = run_replay(args, dist, pk)
     elif args.workload == "similarity":
         line, data = run_similarity(args, dist, pk)
+    elif args.workload == "longtail":
+        line, data = run_longtail(args, dist, pk)
     else:
         line, data = run_lookup(args, dist, pk)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:

@@ -268,32 +268,58 @@ class RolloutEngine:
             for ln, r in zip(lanes, batch_reqs):
                 busy[ln] = r
 
-        def harvest(lanes, to_out=True):
-            if not lanes:
-                return
+        pin = dict(dtype=torch.int32, device="cpu", pin_memory=True)
+        h_len = [torch.empty(n, **pin) for _ in range(2)]
+        h_tgt = [torch.empty(n, **pin) for _ in range(2)]
+        harvests = []              # (event, keys, lanes, pinned tokens [k, stride], pinned stats [k, 5])
+
+        def start_harvest(lanes):
+            """Finished lanes: their rows leave the device asynchronously; the lanes are free at once (any
+            later admission into them is stream-ordered after these copies)."""
+            li = torch.as_tensor(lanes, dtype=torch.long).to(dev, non_blocking=True)
+            toks = torch.empty((len(lanes), state.gen_stride), **pin)
+            sts = torch.empty((len(lanes), 5), dtype=torch.int64, device="cpu", pin_memory=True)
+            toks.copy_(state.gen_tok.index_select(0, li), non_blocking=True)
+            sts.copy_(state.stats.index_select(0, li), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            reqs_ = [busy.pop(ln) for ln in lanes]
+            free.extend(lanes)
+            harvests.append((ev, reqs_, toks, sts))
+
+        def finish_harvests(block=False):
+            while harvests and (block or harvests[0][0].query()):
+                ev, reqs_, toks, sts = harvests.pop(0)
+                ev.synchronize()
+                t, a = toks.numpy(), sts.numpy()
+                for j, r in enumerate(reqs_):
+                    out_tok[r.key] = t[j, :r.target_len].copy()
+                    out_stats[r.key] = a[j].copy()
+
+        def evict(lanes):
+            """Migration: the lanes' state leaves as SeqRequest (synchronous; `on_check` callers only)."""
             li = torch.as_tensor(lanes, dtype=torch.long).to(dev)
             toks = state.gen_tok.index_select(0, li).cpu().numpy()
             sts = state.stats.index_select(0, li).cpu().numpy()
-            if not to_out:
-                win = state.window.index_select(0, li).cpu().numpy()
-                pre = state.prefix_len.index_select(0, li).cpu().numpy()
-                gl = state.gen_len.index_select(0, li).cpu().numpy()
-                state.target_len.index_fill_(0, li, 0)     # the lane stops decoding
+            win = state.window.index_select(0, li).cpu().numpy()
+            pre = state.prefix_len.index_select(0, li).cpu().numpy()
+            gl = state.gen_len.index_select(0, li).cpu().numpy()
+            state.target_len.index_fill_(0, li, 0)     # the lane stops decoding
             for j, ln in enumerate(lanes):
                 r = busy.pop(ln)
-                if to_out:
-                    out_tok[r.key] = toks[j, :r.target_len].copy()
-                    out_stats[r.key] = sts[j].copy()
-                else:
-                    evicted.append(SeqRequest(r.key, r.prompt, r.target_len, r.slot, toks[j, :gl[j]].copy(),
-                                              int(win[j]), int(pre[j]), sts[j].copy()))
+                evicted.append(SeqRequest(r.key, r.prompt, r.target_len, r.slot, toks[j, :gl[j]].copy(),
+                                          int(win[j]), int(pre[j]), sts[j].copy()))
                 free.append(ln)
 
-        while queue or busy:
+        # The host reads the lanes' progress one chunk late: chunk c + 1 is queued before chunk c's gen_len
+        # copy is waited on, so the GPU never drains at a check (a finished lane idles at most two chunks).
+        chunk = 0
+        pending = None
+        while queue or busy or pending is not None:
             if queue and free and (len(free) >= admit_min or not busy or len(queue) <= len(free)):
                 k = min(len(free), len(queue))
                 admit([queue.popleft() for _ in range(k)])
-            if graph is None and self.use_graphs:
+            if busy and graph is None and self.use_graphs:
                 iteration()            # eager first iteration (kernel attributes), then capture
                 it_host += 1
                 busy_iters += len(busy)
@@ -306,21 +332,40 @@ class RolloutEngine:
                 per_iter = launch_count() - c0
                 self.graph_launches -= per_iter
                 st.wait_stream(side)
-            for _ in range(self.check_every):
-                if self.use_graphs:
-                    graph.replay()
-                    self.graph_launches += per_iter
-                else:
-                    iteration()
-            it_host += self.check_every
-            busy_iters += self.check_every * len(busy)
-            gl = state.gen_len.cpu().numpy()
-            tl = state.target_len.cpu().numpy()
-            done = [ln for ln in busy if gl[ln] >= tl[ln]]
-            harvest(done)
-            if on_check is not None and busy:
-                ev = list(on_check({ln: busy[ln].key for ln in busy}, gl, it_host) or [])
-                harvest([ln for ln in ev if ln in busy], to_out=False)
+            snap = None
+            if busy:
+                for _ in range(self.check_every):
+                    if self.use_graphs:
+                        graph.replay()
+                        self.graph_launches += per_iter
+                    else:
+                        iteration()
+                it_host += self.check_every
+                busy_iters += self.check_every * len(busy)
+                b = chunk & 1
+                h_len[b].copy_(state.gen_len, non_blocking=True)
+                h_tgt[b].copy_(state.target_len, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                snap = (ev, b, dict(busy))
+                chunk += 1
+            if pending is not None:
+                ev, b, was_busy = pending
+                ev.synchronize()
+                gl, tl = h_len[b].numpy(), h_tgt[b].numpy()
+                done = [ln for ln, r in was_busy.items() if busy.get(ln) is r and gl[ln] >= tl[ln]]
+                if done:
+                    start_harvest(done)
+                if on_check is not None and busy:
+                    torch.cuda.synchronize(dev)
+                    gl_now = state.gen_len.cpu().numpy()
+                    ev_l = list(on_check({ln: busy[ln].key for ln in busy}, gl_now, it_host) or [])
+                    ev_l = [ln for ln in ev_l if ln in busy and gl_now[ln] < state.target_len[ln].item()]
+                    if ev_l:
+                        evict(ev_l)
+            finish_harvests()
+            pending = snap
+        finish_harvests(block=True)
         ev1.record(st)
         torch.cuda.synchronize(dev)
         a = acc.cpu().numpy()

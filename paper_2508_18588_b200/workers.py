@@ -329,6 +329,30 @@ def plan_allocation(lens, wks: int, t_train: float, model, min_wks: int = 1, max
     return AllocationPlan(best[0], best[1], t0, True)
 
 
+def plan_makespan(lens, wks: int, model, min_wks: int = 1) -> AllocationPlan:
+    """Rollout-only variant of the two-tier allocation: the per-group worker counts that minimise the slowest
+    group's tau (every group's deadline is the same T: workers_for_gradient with d = 0, T the smallest
+    candidate whose plan fits in `wks`).  plan_allocation's staggered deadlines t0 + i * d exist to overlap
+    short groups' training with long groups' rollouts (scheduler.py:224-266); a rollout-throughput
+    benchmark with no training stage wants them all to finish together."""
+    n = len(lens)
+    if n < 1 or wks < n * min_wks:
+        return AllocationPlan([], 0.0, 0.0, False)
+    hi_k = max(min_wks, wks - (n - 1) * min_wks)
+    cands = sorted({model.tau(l, k) for l in lens for k in range(min_wks, hi_k + 1)})
+    for T in cands:
+        total, plan = workers_for_gradient(0.0, lens, T, model, min_wks, hi_k)
+        if total <= wks:
+            # hand spare workers to the groups that gain most (longest first)
+            spare = wks - total
+            for i in sorted(range(n), key=lambda i: -lens[i]):
+                while spare > 0 and model.tau(lens[i], plan[i] + 1) < model.tau(lens[i], plan[i]):
+                    plan[i] += 1
+                    spare -= 1
+            return AllocationPlan(plan, 0.0, T, True)
+    return AllocationPlan([], 0.0, 0.0, False)
+
+
 def assign_with_plan(groups: list, per_group_workers: list, step: int) -> dict:
     """{rank: prompt ids}: group i gets per_group_workers[i] consecutive ranks (the group order alternates
     with the step, scheduler.py:79-88); a group's prompts, in length order, are dealt round-robin over its

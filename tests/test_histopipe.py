@@ -89,3 +89,13 @@ def test_assign_with_plan_alternates_and_covers():
         assert sorted(p for v in a.values() for p in v) == sorted(med)
         assert len(a) == 4
     assert a1[0] == groups[0].prompt_ids and a2[0] == groups[2].prompt_ids[0::2]
+
+
+def test_plan_makespan_balances_groups():
+    m = W.TauProfile.from_rows([(l, k, l / 1000 / k) for l in (512, 2048, 8192, 16384) for k in (1, 2, 3, 4)])
+    p = W.plan_makespan([1500.0, 6000.0], 4, m)
+    assert p.feasible and p.per_group_workers == [1, 3]
+    assert max(m.tau(l, k) for l, k in zip([1500.0, 6000.0], p.per_group_workers)) == pytest.approx(2.0)
+    # the reference's gradient plan gives the short group the workers (its training overlaps the long tail)
+    assert W.plan_allocation([1500.0, 6000.0], 4, 0.0, m, precision=0.01).per_group_workers == [3, 1]
+    assert not W.plan_makespan([1.0, 2.0, 3.0], 2, m).feasible

@@ -27,9 +27,9 @@ def test_pack_rows(torch):
     order = rng.permutation(n).astype(np.int32)
     off = np.concatenate([[0], np.cumsum(lens[order])[:-1]]).astype(np.int64)
     dst = torch.full((int(lens.sum()) + 5,), -7, dtype=torch.int32, device="cuda")
-    d = lambda a: torch.as_tensor(a).cuda()  # noqa: E731
-    _lib.check(lib.hs_pack_rows(src.data_ptr(), stride, d(order).data_ptr(), d(lens[order]).data_ptr(),
-                                d(off).data_ptr(), n, dst.data_ptr(), None))
+    d_order, d_len, d_off = (torch.as_tensor(a).cuda() for a in (order, lens[order], off))   # kept alive
+    _lib.check(lib.hs_pack_rows(src.data_ptr(), stride, d_order.data_ptr(), d_len.data_ptr(), d_off.data_ptr(),
+                                n, dst.data_ptr(), None))
     h = src.cpu().numpy()
     ref = np.concatenate([h[i, :lens[i]] for i in order])
     out = dst.cpu().numpy()
