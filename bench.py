@@ -20,6 +20,7 @@ CUDA events on the launching stream, max over ranks.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -736,9 +737,13 @@ def run_longtail(args, dist, pk):
         plan = (W.plan_makespan(lens_g, world, tau) if args.histopipe == "makespan"
                 else W.plan_allocation(lens_g, world, 0.0, tau, precision=0.01))
         per_group = plan.per_group_workers if plan.feasible else W.partition_sizes(world, n_groups)
-        mine = W.assign_with_plan(groups, per_group, 1)[rank]
+        assign = W.assign_with_plan(groups, per_group, 1)
+        mine = assign[rank]
+        group_of_rank = {r: next(g.index for g in groups if set(assign[r]) <= set(g.prompt_ids))
+                         for r in range(world)}
     else:
         mine = list(range(n_prompts))
+        groups, group_of_rank = None, {0: 0}
     eng = make_engine(tgt[mine].max())
     lanes = eng.n_slots
 
@@ -752,8 +757,75 @@ def run_longtail(args, dist, pk):
     # length-aware admission: longest predicted (the prompt's last-epoch median) first
     order = sorted(range(len(reqs)), key=lambda i: (-med[mine[i // S]], i))
     queue = [reqs[i] for i in order]
+    migrate = bool(args.migrate and world > 1)
+    # last epoch's lengths: this epoch's targets over a per-rollout growth factor; stragglers that outgrow
+    # beta x their group's longest history are the rollouts HistoPipe migrates (scheduler.py:304-330)
+    grow = np.exp(args.growth_sigma * np.random.default_rng([args.seed, 4343]).standard_normal(tgt.shape))
+    hist_len = np.clip(tgt / grow, lo, hi)
+    policy = W.MigrationPolicy(alpha_pct=args.alpha_pct, beta=W.beta_from_history(list(grow.ravel())))
+    run_no = [0]
+    mig_log = {"evicted": 0, "received": 0}
+
+    def run_epoch(idx_, spec_on):
+        """One epoch of this rank's requests; with --migrate, stragglers move between ranks mid-epoch."""
+        if not migrate:
+            return eng.rollout_stream(queue, index=idx_, speculate=spec_on)
+        run_no[0] += 1
+        broker = W.MigrationBroker(dist.pg.distributed_c10d._get_default_store(), rank, world,
+                                   tag="mig%d" % run_no[0])
+        dist.barrier()
+        g_me = group_of_rank[rank]
+        max_hist = float(max(hist_len[p].max() for p in groups[g_me].prompt_ids))
+        total = len(queue)
+        done_keys = set()
+
+        def on_check(live, gl, it, waiting):
+            remaining = waiting + len(live)
+            left = sum(max(0, queue_t[k] - int(gl[ln])) for ln, k in live.items())
+            broker.publish_load(left)
+            loads = broker.loads()
+            act = {}
+            for r, ld in loads.items():
+                if r != rank and ld > 0:
+                    act[group_of_rank[r]] = act.get(group_of_rank[r], 0.0) + ld
+            out = []
+            for ln, k in live.items():
+                kind, tg = W.migration_decision(g_me, max_hist, int(gl[ln]), total - remaining, total, policy,
+                                                len(groups), act)
+                if kind == "intra_step" and tg is not None:
+                    dst = min((loads.get(r, 0.0), r) for r in range(world) if group_of_rank[r] == tg)[1]
+                    out.append(ln)
+                    dest[k] = dst
+            return out
+
+        def on_evict(req):
+            mig_log["evicted"] += 1
+            broker.post(dest.pop(req.key), req)
+
+        def inbox():
+            # a migrated-in rollout continues without drafts: its history slot indexes the source GPU's
+            # GpuIndex (the receiving engine's graph holds this rank's index)
+            got = [dataclasses.replace(r, slot=-1) for r in broker.poll()]
+            mig_log["received"] += len(got)
+            return got
+
+        dest = {}
+        res_ = eng.rollout_stream(queue, index=idx_, speculate=spec_on, on_check=on_check, on_evict=on_evict,
+                                  inbox=inbox, keep_alive=broker.keep_alive, max_target=hi)
+        dist.barrier()
+        return res_
+
+    queue_t = {r.key: r.target_len for r in reqs}
     # epoch 1: plain rollouts (the speculation-off baseline and the truth the speculative epochs reproduce)
-    base = eng.rollout_stream(queue, speculate=False)
+    base = run_epoch(None, False)
+    if migrate:   # rollouts that finished on another rank come home (host exchange of the few migrated ones)
+        import torch.distributed as tdist
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, {k: v for k, v in base.tokens.items() if k not in queue_t})
+        for part in gathered:
+            for k, v in part.items():
+                if k in queue_t:
+                    base.tokens[k] = v
     n_tok = int(sum(targets))
     truth = np.concatenate([base.tokens[k] for k in keys]).astype(np.int32)
     resp_off = np.concatenate([[0], np.cumsum(targets)]).astype(np.int64)
@@ -777,15 +849,30 @@ def run_longtail(args, dist, pk):
         box = {}
 
         def step():
-            box["res"] = eng.rollout_stream(queue, index=idx, speculate=True)
+            box["res"] = run_epoch(idx, True)
 
         lc0, mc0, gl0 = lib_hs.hs_launch_count(), mlib().hm_launch_count(), eng.graph_launches
         e2e_ms, clocks = timed(step, args.steps, args.warmup if si == 0 else 1, dist, stream, dist.local)
         launches = ((lib_hs.hs_launch_count() - lc0) + (mlib().hm_launch_count() - mc0)
                     + (eng.graph_launches - gl0)) // (args.steps + (args.warmup if si == 0 else 1))
         res = box["res"]
-        exact = all(np.array_equal(res.tokens[k], base.tokens[k]) for k in keys)
-        st = np.sum([res.stats[k] for k in keys], axis=0)
+        if migrate:   # every rollout finished somewhere: check it against its owner's epoch-1 output
+            import hashlib
+            import torch.distributed as tdist
+            mine_h = {k: hashlib.sha1(np.ascontiguousarray(v, np.int32).tobytes()).hexdigest()
+                      for k, v in res.tokens.items()}
+            base_h = {k: hashlib.sha1(np.ascontiguousarray(base.tokens[k], np.int32).tobytes()).hexdigest()
+                      for k in keys}
+            ga, gb = [None] * world, [None] * world
+            tdist.all_gather_object(ga, mine_h)
+            tdist.all_gather_object(gb, base_h)
+            fin = {k: h for part in ga for k, h in part.items()}
+            ref = {k: h for part in gb for k, h in part.items()}
+            exact = fin == ref
+            st = np.sum(list(res.stats.values()), axis=0)
+        else:
+            exact = all(np.array_equal(res.tokens[k], base.tokens[k]) for k in keys)
+            st = np.sum([res.stats[k] for k in keys], axis=0)
         value = dist.sum(n_tok) / (dist.max(e2e_ms) / 1e3)
         row = {"similarity": sim, "value": value, "ms_per_step": e2e_ms,
                "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
@@ -845,6 +932,10 @@ def run_longtail(args, dist, pk):
         "clocks": clocks,
         "sweep": rows,
         "ranks": ranks,
+        "migration": {"enabled": migrate, "alpha_pct": args.alpha_pct, "beta": policy.beta,
+                      "evicted_rank0": mig_log["evicted"], "received_rank0": mig_log["received"],
+                      "note": "intra-step straggler migration (scheduler.py:304-330) with KV recompute by prefill "
+                              "on the receiving GPU; history lengths = targets / exp(%.2f z)" % args.growth_sigma},
         "static_waves_value": (dist.sum(n_tok) / dist.max(waves_ms / 1e3)) if waves_ms else None,
         "occupancy": row["occupancy"],
         "nonspec_value": nonspec,
@@ -1045,6 +1136,9 @@ def main():
     ap.add_argument("--similarity-sweep", default="", help="longtail: comma-separated similarities")
     ap.add_argument("--compare-waves", action="store_true", help="longtail: also time static waves")
     ap.add_argument("--kv-gb", type=float, default=120.0, help="longtail: KV-cache budget per GPU (GB)")
+    ap.add_argument("--migrate", action="store_true", help="longtail: intra-step straggler migration")
+    ap.add_argument("--alpha-pct", type=float, default=10.0, help="longtail: migration alpha (percent)")
+    ap.add_argument("--growth-sigma", type=float, default=0.25, help="longtail: epoch length-growth noise")
     ap.add_argument("--histopipe", default="makespan", choices=["makespan", "gradient"],
                     help="longtail: per-group GPU plan (gradient = the reference's plan_allocation)")
     ap.add_argument("--attention", default="tcgen05", choices=["tcgen05", "mma_sync"],

@@ -169,13 +169,18 @@ class RolloutEngine:
             rows += m
         return first, rows
 
-    def rollout_stream(self, requests, index=None, speculate=True, admit_min=None, on_check=None):
+    def rollout_stream(self, requests, index=None, speculate=True, admit_min=None, on_check=None, inbox=None,
+                       keep_alive=None, max_target=None, on_evict=None):
         """Continuous batching: every engine lane runs a sequence; finished lanes are refilled from the
         request queue (in the given order -- the caller puts the predicted-longest first) by an admission
         prefill between CUDA-graph replays, so a long tail does not idle the batch.
 
-        on_check(busy: {lane: key}, gen_len: np.ndarray, iteration) -> lanes to evict, called every
-        `check_every` iterations: their state leaves as SeqRequest (migration with KV recompute).
+        on_check(busy: {lane: key}, gen_len: np.ndarray, iteration, waiting) -> lanes to evict, called every
+        `check_every` iterations with the lanes' progress (one chunk old): their state leaves as SeqRequest
+        (migration with KV recompute).  inbox() -> SeqRequests that arrived (migrated in from other
+        workers) is polled at every check; while keep_alive() is true an idle engine keeps polling.
+        max_target bounds the target length of requests that may still arrive.  on_evict(req) receives each
+        evicted rollout as soon as its state is read (otherwise they are returned in StreamResult.evicted).
         """
         import collections
         import torch
@@ -187,7 +192,7 @@ class RolloutEngine:
         n = self.n_slots
         dev = self.device
         cfgs = self.spec
-        max_t = max([int(r.target_len) for r in reqs] + [1])
+        max_t = max([int(r.target_len) for r in reqs] + [1, int(max_target or 0)])
         max_ctx = max([len(r.prompt) + int(r.target_len) for r in reqs] + [1])
         if max_ctx > self.max_len:
             raise ValueError("prompt + target exceeds max_len")
@@ -307,15 +312,27 @@ class RolloutEngine:
             state.target_len.index_fill_(0, li, 0)     # the lane stops decoding
             for j, ln in enumerate(lanes):
                 r = busy.pop(ln)
-                evicted.append(SeqRequest(r.key, r.prompt, r.target_len, r.slot, toks[j, :gl[j]].copy(),
-                                          int(win[j]), int(pre[j]), sts[j].copy()))
+                req = SeqRequest(r.key, r.prompt, r.target_len, r.slot, toks[j, :gl[j]].copy(), int(win[j]),
+                                 int(pre[j]), sts[j].copy())
+                if on_evict is not None:
+                    on_evict(req)
+                else:
+                    evicted.append(req)
                 free.append(ln)
 
         # The host reads the lanes' progress one chunk late: chunk c + 1 is queued before chunk c's gen_len
         # copy is waited on, so the GPU never drains at a check (a finished lane idles at most two chunks).
         chunk = 0
         pending = None
-        while queue or busy or pending is not None:
+        import time as _time
+        while True:
+            if inbox is not None:
+                queue.extend(inbox())
+            if not (queue or busy or pending is not None):
+                if keep_alive is None or not keep_alive():
+                    break
+                _time.sleep(0.002)
+                continue
             if queue and free and (len(free) >= admit_min or not busy or len(queue) <= len(free)):
                 k = min(len(free), len(queue))
                 admit([queue.popleft() for _ in range(k)])
@@ -357,10 +374,8 @@ class RolloutEngine:
                 if done:
                     start_harvest(done)
                 if on_check is not None and busy:
-                    torch.cuda.synchronize(dev)
-                    gl_now = state.gen_len.cpu().numpy()
-                    ev_l = list(on_check({ln: busy[ln].key for ln in busy}, gl_now, it_host) or [])
-                    ev_l = [ln for ln in ev_l if ln in busy and gl_now[ln] < state.target_len[ln].item()]
+                    live = {ln: busy[ln].key for ln in busy if ln in was_busy and gl[ln] < tl[ln]}
+                    ev_l = [ln for ln in (on_check(live, gl, it_host, len(queue)) or []) if ln in live]
                     if ev_l:
                         evict(ev_l)
             finish_harvests()

@@ -407,3 +407,60 @@ def migration_decision(group_index: int, group_max_hist_len: float, generated_le
         if cands:
             return "intra_step", cands[0][1]
     return "inter_step", None
+
+
+class MigrationBroker:
+    """Hands straggler rollouts between GPU workers mid-step (intra-step migration, sim.py:719-779) through
+    the process group's key-value store: a sender posts the evicted rollout's state (tokens generated so far,
+    AIMD window, prefix length, SpecStats -- engine.SeqRequest) to the receiver's mailbox; the receiver's
+    engine polls it between CUDA-graph replays and re-admits the rollout, recomputing its KV by prefill.
+
+    Termination: a worker may stop only when every worker is idle and every posted rollout was taken
+    (an idle worker marks itself busy before it takes a message, so the check cannot pass in between)."""
+
+    def __init__(self, store, rank: int, world: int, tag: str = "mig"):
+        self.store, self.rank, self.world, self.tag = store, rank, world, tag
+        self.read = 0
+        self.store.set(f"{tag}/idle/{rank}", "0")
+
+    def post(self, dst: int, req) -> None:
+        import pickle
+        self.store.add(f"{self.tag}/posted", 1)
+        n = self.store.add(f"{self.tag}/box/{dst}/n", 1) - 1
+        self.store.set(f"{self.tag}/box/{dst}/{n}", pickle.dumps(req))
+
+    def poll(self) -> list:
+        import pickle
+        n = self.store.add(f"{self.tag}/box/{self.rank}/n", 0)
+        out = []
+        while self.read < n:
+            key = f"{self.tag}/box/{self.rank}/{self.read}"
+            self.store.wait([key])
+            out.append(pickle.loads(self.store.get(key)))
+            self.read += 1
+        if out:
+            self.store.set(f"{self.tag}/idle/{self.rank}", "0")
+            self.store.add(f"{self.tag}/taken", len(out))
+        return out
+
+    def publish_load(self, remaining_tokens: float) -> None:
+        self.store.set(f"{self.tag}/load/{self.rank}", repr(float(remaining_tokens)))
+
+    def loads(self) -> dict:
+        out = {}
+        for r in range(self.world):
+            key = f"{self.tag}/load/{r}"
+            if self.store.check([key]):
+                out[r] = float(self.store.get(key))
+        return out
+
+    def keep_alive(self) -> bool:
+        """Called by an idle engine: True while another worker may still hand it work."""
+        self.store.set(f"{self.tag}/idle/{self.rank}", "1")
+        if self.store.add(f"{self.tag}/box/{self.rank}/n", 0) > self.read:
+            return True
+        idle = all(self.store.get(f"{self.tag}/idle/{r}") == b"1" for r in range(self.world)
+                   if self.store.check([f"{self.tag}/idle/{r}"]))
+        if not idle:
+            return True
+        return self.store.add(f"{self.tag}/posted", 0) != self.store.add(f"{self.tag}/taken", 0)

@@ -71,7 +71,7 @@ def test_migration_with_kv_recompute(setup):
                                device="cuda", check_every=4)
     a, b = mk(), mk()
 
-    def on_check(busy, gen_len, it):
+    def on_check(busy, gen_len, it, waiting):
         return [ln for ln in busy if gen_len[ln] >= 40]
 
     r1 = a.rollout_stream(_reqs(S), index=S["idx"], speculate=True, admit_min=1, on_check=on_check)

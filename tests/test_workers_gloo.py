@@ -98,3 +98,40 @@ def test_route_meta_exchange_world2():
         assert out[rank][1] == expect
         assert [c[1] for c in out[rank][2]] == [sum(r[2] for r in out[src][0] if owner[r[0]] == rank)
                                                 for src in range(world)]
+
+
+def _broker_worker(rank, world, port, out):
+    import time
+
+    import torch.distributed as dist
+    from torch.distributed import distributed_c10d as c10d
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b = W.MigrationBroker(c10d._get_default_store(), rank, world, tag="t")
+    dist.barrier()
+    got = []
+    if rank == 0:
+        for i in range(3):
+            b.post(1, {"key": i, "tokens": list(range(i + 1))})
+            time.sleep(0.05)
+    t0 = time.time()
+    while True:
+        got += b.poll()
+        if not b.keep_alive():
+            break
+        assert time.time() - t0 < 30, "broker never terminated"
+        time.sleep(0.01)
+    out[rank] = got
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_migration_broker_delivers_and_terminates():
+    """MigrationBroker (intra-step migration transport): every posted rollout is taken exactly once by its
+    destination and no worker stops while a message is in flight."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_broker_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out[0] == []
+    assert [m["key"] for m in out[1]] == [0, 1, 2] and out[1][2]["tokens"] == [0, 1, 2]
