@@ -423,19 +423,36 @@ def run_rollout(args, dist, pk):
     B, S, P, T, G = args.batch, args.samples, args.prompt_len, args.length, 8
     per_wave = B // S                   # prompts per wave
     n_waves = args.waves
-    world, rank = dist.world, dist.rank
-    w = Weights(cfg, dev, seed=args.seed)
+    # tensor parallelism (configs[4]): ranks 2g, 2g + 1 form rollout worker g; data parallelism over workers
+    tp = args.tp
+    if dist.world % tp:
+        raise ValueError("--gpus must be a multiple of --tp")
+    world, rank = dist.world // tp, dist.rank // tp          # data-parallel workers
+    tp_group, dp_group = None, None
+    if tp > 1:
+        import torch.distributed as tdist
+        for g in range(world):
+            pg = tdist.new_group([g * tp + t for t in range(tp)])
+            if g == rank:
+                tp_group = pg
+        for t in range(tp):
+            pg = tdist.new_group([g * tp + t for g in range(world)])
+            if t == dist.rank % tp:
+                dp_group = pg
+    w = Weights(cfg, dev, seed=args.seed, tp_rank=dist.rank % tp, tp_size=tp)
     bcast_ms = None
-    if world > 1:   # epoch boundary: the updated policy travels from rank 0 (NCCL over NVLink)
-        for _ in range(2):   # first call includes communicator setup; report the warm one
+    bcast_gbps = None
+    if world > 1:   # epoch boundary: the updated policy travels from worker 0 (one NCCL call over NVLink)
+        for _ in range(3):   # first call includes communicator setup; report the warm one
             dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            W.broadcast_weights(w, src=0)
+            W.broadcast_weights(w, src=dist.rank % tp, group=dp_group)
             torch.cuda.synchronize()
             bcast_ms = 1e3 * (time.perf_counter() - t0)
-    eng = RolloutEngine(cfg, w, n_slots=B, max_len=P + T, device=dev, attention=args.attention,
-                        temperature=args.temperature, seed=args.seed)
+        bcast_gbps = w.flat.numel() * 2 / (bcast_ms / 1e3) / 1e9
+    eng = RolloutEngine(w.cfg, w, n_slots=B, max_len=P + T, device=dev, attention=args.attention,
+                        temperature=args.temperature, seed=args.seed, tp_group=tp_group)
 
     def prompt_tokens(pid):
         return np.random.default_rng([args.seed, 1000 + pid]).integers(0, cfg.vocab, size=P, dtype=np.int32)
@@ -526,7 +543,8 @@ def run_rollout(args, dist, pk):
         d_tokens.record_stream(side_st)
         with torch.cuda.stream(side_st):
             return W.route_rollouts_device(d_tokens, np.full(B, T, np.int64), seq_pid, keys,
-                                           np.full(B, 1 << 32, np.int64), owner, rank, world, stream=side_st)
+                                           np.full(B, 1 << 32, np.int64), owner, rank, world, stream=side_st,
+                                           group=dp_group)
 
     # epoch 1 -> epoch 2: route the plain rollouts and build every wave's epoch-2 history
     waves = []
@@ -573,8 +591,9 @@ def run_rollout(args, dist, pk):
     st = np.sum([r.stats.sum(axis=0) for r in timed_res], axis=0)
     res = timed_res[-1]
     gen = B * T
-    value = dist.sum(gen) / (ms_dev / 1e3)
-    e2e = dist.sum(gen) / (e2e_ms / 1e3)
+    # tokens of a tensor-parallel worker are counted once (its tp ranks hold the same rollouts)
+    value = dist.sum(gen) / tp / (ms_dev / 1e3)
+    e2e = dist.sum(gen) / tp / (e2e_ms / 1e3)
     # step roofline (aggregate bound: max of total bytes / HBM and total flops / sustained bf16)
     bytes_total = res.forwards * res.weight_bytes + res.kv_bytes
     t_roof = max(bytes_total / (pk["hbm_gbs"] * 1e9), res.flops / (pk["bf16_tflops_sustained"] * 1e12))
@@ -632,11 +651,13 @@ def run_rollout(args, dist, pk):
                                    2 if sampling else 1, cfg.name, per_wave, S, B, P, T,
                                    "sampled" if sampling else "greedy", per_wave * n_waves),
                    "step": "one wave: K1 ingest of its history + the HistoSpec rollout + routing of its outputs",
-                   "parallelism": "dp%d (independent rollout workers)" % dist.world,
+                   "parallelism": ("dp%d (independent rollout workers)" % world) if tp == 1 else
+                                  "dp%d x tp%d (each worker a GPU pair; O / down all-reduced over peer memory)" % (
+                                      world, tp),
                    "l2": "KV cache (%.0f GB) and weights stream far beyond the 126 MB L2" % (
                        eng.cache.buf.numel() * 2 / 1e9)},
         "attention_family": args.attention,
-        "collectives": {"weight_broadcast_ms": bcast_ms, "rollout_route_ms_per_step": float(np.mean(
+        "collectives": {"weight_broadcast_ms": bcast_ms, "weight_broadcast_GBps": bcast_gbps, "rollout_route_ms_per_step": float(np.mean(
             acc["route_ms"][-args.steps:])), "note": "epoch-boundary only: NCCL broadcast of the policy, "
                                                      "all-to-all-v of finished rollouts to next-step owners"},
         "ingest_ms_per_step": float(np.mean([a.elapsed_time(b) for a, b in acc["ingest_ms"][-args.steps:]])),
@@ -651,16 +672,16 @@ def run_rollout(args, dist, pk):
         "side_file": side,
         "clocks": clocks,
         # the speculation result last, where a truncated log tail still shows it
-        "nonspec_value_%s" % other: dist.sum(B * T) / dist.max(base_other.gpu_ms / 1e3),
-        "nonspec_value": dist.sum(B * T) / dist.max(float(np.mean(base_ms)) / 1e3),
+        "nonspec_value_%s" % other: dist.sum(B * T) / tp / dist.max(base_other.gpu_ms / 1e3),
+        "nonspec_value": dist.sum(B * T) / tp / dist.max(float(np.mean(base_ms)) / 1e3),
         "engine_iterations": float(np.mean([r.iterations for r in timed_res])),
         "acceptance_rate": float(st[2] / max(st[1], 1)),
         "tokens_per_iteration": float(st[0] / max(st[3] + st[4], 1)),
         "mean_accepted_per_verify": float(st[2] / max(st[3], 1)),
         ("bit_exact_vs_plain_sampling" if sampling else "bit_exact_vs_greedy"):
-            bool(dist.sum(float(acc["exact"])) == world),
-        "speedup_vs_nonspec": value / max(dist.sum(B * T) / dist.max(float(np.mean(base_ms)) / 1e3),
-                                          dist.sum(B * T) / dist.max(base_other.gpu_ms / 1e3), 1e-9),
+            bool(dist.sum(float(acc["exact"])) == dist.world),
+        "speedup_vs_nonspec": value / max(dist.sum(B * T) / tp / dist.max(float(np.mean(base_ms)) / 1e3),
+                                          dist.sum(B * T) / tp / dist.max(base_other.gpu_ms / 1e3), 1e-9),
     }
     return line, {"cfg": cfg, "prompts": waves[0]["h_prompts"].numpy(), "T": T, "w": w}
 
@@ -731,6 +752,12 @@ def run_longtail(args, dist, pk):
         groups = W.build_groups({p: float(med[p]) for p in range(n_prompts)}, n_groups)
         probe = make_engine(hi)
         tau = tau_profile(probe, cfg, world, probe.n_slots, len(groups[0].prompt_ids) * S, pk, dist)
+        if rank == 0:
+            try:
+                os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+                tau.to_csv(os.path.join(ROOT, "gpurun_out", "tau_profile_%s_%dgpu.csv" % (cfg.name, world)))
+            except OSError:
+                pass
         del probe
         torch.cuda.empty_cache()
         lens_g = [g.representative_len for g in groups]
@@ -1136,6 +1163,7 @@ def main():
     ap.add_argument("--similarity-sweep", default="", help="longtail: comma-separated similarities")
     ap.add_argument("--compare-waves", action="store_true", help="longtail: also time static waves")
     ap.add_argument("--kv-gb", type=float, default=120.0, help="longtail: KV-cache budget per GPU (GB)")
+    ap.add_argument("--tp", type=int, default=1, choices=[1, 2], help="rollout: tensor-parallel GPUs per worker")
     ap.add_argument("--migrate", action="store_true", help="longtail: intra-step straggler migration")
     ap.add_argument("--alpha-pct", type=float, default=10.0, help="longtail: migration alpha (percent)")
     ap.add_argument("--growth-sigma", type=float, default=0.25, help="longtail: epoch length-growth noise")

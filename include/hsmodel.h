@@ -127,6 +127,15 @@ int hm_attention_family(void);
  * changes only which CTA computes a tile, never a tile's arithmetic (bits are unchanged). */
 int hm_set_grid_caps(int32_t gemm_ctas, int32_t attn_ctas);
 
+/* Tensor parallelism over a GPU pair (configs[4]).
+ * hm_rmsnorm_residual2: x += (y + y2) then rmsnorm, any d (y2 optional: the peer GPU's fp32 partial of the
+ * O / down projection, read in place over NVLink from its symmetric buffer -- the all-reduce fused into the
+ * norm).  hm_tp_barrier: stream-ordered two-GPU barrier over peer memory (system fence, release store of
+ * this GPU's generation into the peer's flag, acquire spin on its own flag); graph-capturable. */
+int hm_rmsnorm_residual2(float* d_x, const float* d_y, const float* d_y2, const void* d_w, int32_t M, int32_t d,
+                         float eps, void* d_out, const int32_t* d_m, hm_stream_t stream);
+int hm_tp_barrier(int32_t* d_my_flag, int32_t* d_peer_flag, int32_t* d_gen, hm_stream_t stream);
+
 /* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent): the
  * per-sequence tile prefix and, for the tcgen05 family, each tile's sequence.  d_work holds
  * hm_attention_work_size(n_seq, max_q_len, H, KVH) int32 values. */

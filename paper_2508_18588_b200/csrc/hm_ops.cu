@@ -131,6 +131,76 @@ __global__ void k_rmsnorm_residual(float* __restrict__ x, const float* __restric
   }
 }
 
+// Any d (two passes, the row is re-read from x instead of held in registers) and an optional second partial:
+// x += (y + y2), the tensor-parallel all-reduce of the O / down projections folded into the norm -- y is this
+// GPU's partial, y2 the peer's, read over NVLink from its symmetric buffer.  y + y2 is the same fp32 sum on
+// both GPUs (commutative), so the replicated residual stream stays bit-identical across the pair.  Same
+// per-lane reduction order as k_rmsnorm / k_rmsnorm_residual (column i = lane + 32 k).
+__global__ void k_rmsnorm_residual_g(float* __restrict__ x, const float* __restrict__ y, const float* y2,
+                                     const __nv_bfloat16* __restrict__ w, int M, int d, float eps, const int* m_dev,
+                                     __nv_bfloat16* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int m = m_dev ? *m_dev : M;
+  const int nv = d / 4;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    float4* xr = reinterpret_cast<float4*>(x + (size_t)row * d);
+    const float4* yr = y ? reinterpret_cast<const float4*>(y + (size_t)row * d) : nullptr;
+    const float4* y2r = y2 ? reinterpret_cast<const float4*>(y2 + (size_t)row * d) : nullptr;
+    float ss = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+      float4 a = xr[i];
+      if (yr) {
+        float4 b = yr[i];
+        if (y2r) {
+          const float4 c = y2r[i];
+          b.x += c.x;
+          b.y += c.y;
+          b.z += c.z;
+          b.w += c.w;
+        }
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+        xr[i] = a;
+      }
+      ss += a.x * a.x;
+      ss += a.y * a.y;
+      ss += a.z * a.z;
+      ss += a.w * a.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float r = rsqrtf(ss / (float)d + eps);
+    __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * d);
+    const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(w);
+    for (int i = lane; i < nv; i += 32) {
+      const float4 v = xr[i];
+      const float2 wa = __bfloat1622float2(w2[2 * i]), wb = __bfloat1622float2(w2[2 * i + 1]);
+      orow[2 * i] = __floats2bfloat162_rn(v.x * r * wa.x, v.y * r * wa.y);
+      orow[2 * i + 1] = __floats2bfloat162_rn(v.z * r * wb.x, v.w * r * wb.y);
+    }
+  }
+}
+
+// Two-GPU barrier over peer memory (tensor-parallel pair): bump this GPU's generation, publish it in the
+// peer's flag word (system-scope release after a system fence: every write this stream made before -- the
+// GEMM's partial in the symmetric buffer -- is visible to the peer first), then wait until the peer's
+// generation reached ours.  Stream-ordered and graph-capturable (the generation lives in device memory).
+__global__ void k_tp_barrier(int* my_flag, int* peer_flag, int* gen) {
+  if (threadIdx.x != 0) return;
+  const int g = *gen + 1;
+  *gen = g;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(peer_flag), "r"(g) : "memory");
+  int v;
+  do {
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
+  } while (v < g);
+  __threadfence_system();
+}
+
 // block per row (grid-stride): threads cover the 16-byte chunks of q/k rotations and v copies
 __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const int32_t* __restrict__ pos,
                           const int32_t* __restrict__ row_slot, const float* __restrict__ cosb,
@@ -320,6 +390,27 @@ extern "C" int hm_rmsnorm_residual(float* d_x, const float* d_y, const void* d_w
   else if (nv <= 16) hm::k_rmsnorm_residual<16><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
   else if (nv <= 24) hm::k_rmsnorm_residual<24><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
   else hm::k_rmsnorm_residual<32><<<grid, block, 0, st>>>(d_x, d_y, w, M, d, eps, d_m, out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_rmsnorm_residual2(float* d_x, const float* d_y, const float* d_y2, const void* d_w, int32_t M,
+                                    int32_t d, float eps, void* d_out, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (d % 4) { hm_set_error("rmsnorm_residual2: d % 4 == 0"); return HM_ERR_INVALID; }
+  if (d_y2 && !d_y) { hm_set_error("rmsnorm_residual2: y2 needs y"); return HM_ERR_INVALID; }
+  if (!d_y2 && d <= 4096) return hm_rmsnorm_residual(d_x, d_y, d_w, M, d, eps, d_out, d_m, stream);
+  const int rows = 8;
+  hm::k_rmsnorm_residual_g<<<(M + rows - 1) / rows < 1184 ? (M + rows - 1) / rows : 1184, 32 * rows, 0,
+                             (cudaStream_t)stream>>>(d_x, d_y, d_y2, (const __nv_bfloat16*)d_w, M, d, eps, d_m,
+                                                     (__nv_bfloat16*)d_out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_tp_barrier(int32_t* d_my_flag, int32_t* d_peer_flag, int32_t* d_gen, hm_stream_t stream) {
+  if (!d_my_flag || !d_peer_flag || !d_gen) { hm_set_error("hm_tp_barrier: null pointer"); return HM_ERR_INVALID; }
+  hm::k_tp_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(d_my_flag, d_peer_flag, d_gen);
   HM_LAUNCH_CHECK();
   return HM_OK;
 }

@@ -52,7 +52,10 @@ class RolloutResult:
 class RolloutEngine:
     def __init__(self, cfg: ModelConfig, weights: Weights, n_slots: int, max_len: int, device,
                  spec: SpecConfig | None = None, prefill_rows: int = 16384, use_graphs: bool = True,
-                 check_every: int = 8, temperature: float = 0.0, seed: int = 0, attention: str | None = None):
+                 check_every: int = 8, temperature: float = 0.0, seed: int = 0, attention: str | None = None,
+                 tp_group=None):
+        """tp_group: the process group of a tensor-parallel pair; `weights` is then this GPU's shard
+        (Weights(tp_rank, tp_size)) and `cfg` its local shape (weights.cfg)."""
         import torch
         # attention kernel family ("tcgen05" or "mma_sync"; None: the library default), set per rollout
         self.attention = attention
@@ -68,6 +71,9 @@ class RolloutEngine:
         # accept a point-mass draft x iff the row's sample equals x (probability p(x)), else emit the
         # sample, which is then distributed as p restricted to tokens != x (hm_lm_head_sample)
         self.fwd.temperature, self.fwd.seed = float(temperature), int(seed)
+        if tp_group is not None:
+            from .tp import TensorParallel
+            self.fwd.tp = TensorParallel(tp_group, self.fwd.max_rows, cfg.d_model, self.device)
         self.prefill_rows = prefill_rows
         i32 = dict(dtype=torch.int32, device=self.device)
         R = self.fwd.max_rows

@@ -46,6 +46,8 @@ SIGNATURES = {
     "hm_set_attention_family": [_I32],
     "hm_set_grid_caps": [_I32, _I32],
     "hm_set_gemm_pair": [_I32],
+    "hm_rmsnorm_residual2": [_P, _P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
+    "hm_tp_barrier": [_P, _P, _P, _P],
     "hm_f32_gemm": [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _I32, _P],
     "hm_f32_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P],
     "hm_f32_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P],
@@ -134,7 +136,20 @@ class ModelConfig:
 TINY = ModelConfig("tiny-2L-d256", 2, 256, 4, 4, 64, 1024, 4096, True)
 QWEN25_1P5B = ModelConfig("qwen2.5-1.5b-shape", 28, 1536, 12, 2, 128, 8960, 151936, True)
 QWEN25_7B = ModelConfig("qwen2.5-7b-shape", 28, 3584, 28, 4, 128, 18944, 152064, False)
-PRESETS = {c.name: c for c in (TINY, QWEN25_1P5B, QWEN25_7B)}
+QWEN25_32B = ModelConfig("qwen2.5-32b-shape", 64, 5120, 40, 8, 128, 27648, 152064, False)
+PRESETS = {c.name: c for c in (TINY, QWEN25_1P5B, QWEN25_7B, QWEN25_32B)}
+
+
+def tp_local_config(cfg: ModelConfig, tp_size: int) -> ModelConfig:
+    """One GPU's share of a tensor-parallel group: q / kv heads and FFN columns split evenly (Megatron-style
+    column-parallel QKV and gate/up, row-parallel O and down); embeddings, norms and the LM head replicated."""
+    if tp_size == 1:
+        return cfg
+    if cfg.n_heads % tp_size or cfg.n_kv_heads % tp_size or cfg.ffn % (tp_size * 128):
+        raise ValueError(f"{cfg.name}: heads, kv heads and ffn/128 must divide by tp={tp_size}")
+    import dataclasses
+    return dataclasses.replace(cfg, name=f"{cfg.name}-tp{tp_size}", n_heads=cfg.n_heads // tp_size,
+                               n_kv_heads=cfg.n_kv_heads // tp_size, ffn=cfg.ffn // tp_size)
 
 
 def gemm_bn(n: int) -> int:
@@ -160,9 +175,15 @@ def interleave_gate_up(gate, up, tile=None):
 class Weights:
     """Random-init bf16 weights on `device` (seeded, generated on the device)."""
 
-    def __init__(self, cfg: ModelConfig, device, seed: int = 0, keep_fp32_split: bool = False):
+    def __init__(self, cfg: ModelConfig, device, seed: int = 0, keep_fp32_split: bool = False, tp_rank: int = 0,
+                 tp_size: int = 1):
+        """tp_size > 1: this GPU's shard of the same seeded weights (the full tensors are generated in the
+        TP=1 order, one layer at a time, and sliced); `cfg` becomes the local shape, `global_cfg` the model."""
         import torch
-        self.cfg = cfg
+        self.global_cfg = cfg
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        cfg_l = tp_local_config(cfg, tp_size)
+        self.cfg = cfg_l
         g = torch.Generator(device=device)
         g.manual_seed(seed)
         std = cfg.init_std
@@ -174,16 +195,33 @@ class Weights:
         self.embed = rnd(cfg.vocab, d)
         self.lm_head = self.embed if cfg.tied else rnd(cfg.vocab, d)
         self.layers = []
+        t = tp_rank
+        Hq, Hk, F = cfg_l.n_heads * hd, cfg_l.n_kv_heads * hd, cfg_l.ffn
+
+        def qkv_rows(a):   # this rank's q heads, k heads, v heads (column-parallel QKV)
+            if tp_size == 1:
+                return a
+            q0, k0, v0 = 0, cfg.n_heads * hd, (cfg.n_heads + cfg.n_kv_heads) * hd
+            return torch.cat([a[q0 + t * Hq:q0 + (t + 1) * Hq], a[k0 + t * Hk:k0 + (t + 1) * Hk],
+                              a[v0 + t * Hk:v0 + (t + 1) * Hk]]).contiguous()
+
+        def cols(a, n):    # this rank's slice of the K dimension (row-parallel O / down)
+            return a if tp_size == 1 else a[:, t * n:(t + 1) * n].contiguous()
+
+        def rows(a, n):
+            return a if tp_size == 1 else a[t * n:(t + 1) * n].contiguous()
+
         for _ in range(cfg.n_layers):
             gate, up = rnd(cfg.ffn, d), rnd(cfg.ffn, d)
+            gate, up = rows(gate, F), rows(up, F)
             layer = {
                 "ln1": torch.ones(d, dtype=torch.bfloat16, device=device),
-                "wqkv": rnd(cfg.qkv_dim, d),
-                "bqkv": rnd(cfg.qkv_dim),
-                "wo": rnd(d, cfg.n_heads * hd),
+                "wqkv": qkv_rows(rnd(cfg.qkv_dim, d)),
+                "bqkv": qkv_rows(rnd(cfg.qkv_dim)),
+                "wo": cols(rnd(d, cfg.n_heads * hd), Hq),
                 "ln2": torch.ones(d, dtype=torch.bfloat16, device=device),
                 "wgu": interleave_gate_up(gate, up),
-                "wd": rnd(d, cfg.ffn),
+                "wd": cols(rnd(d, cfg.ffn), F),
             }
             if keep_fp32_split:
                 layer["gate"], layer["up"] = gate, up
@@ -286,6 +324,7 @@ class Forward:
         # and the norms that follow read x alone; False: they store fp32 and the next norm adds (same bits)
         self.residual_in_gemm = os.environ.get("HM_RESIDUAL_IN_GEMM", "0") == "1"
         self.seed = 0
+        self.tp = None   # tp.TensorParallel: O / down partials all-reduced over peer memory (set by the engine)
 
     def run(self, M, tokens, pos, row_slot, q_off, q_len, pos0, kv_slot, n_seq, max_q_len, stream=None, m_dev=None,
             logits_out=None, prof=None, row_key=None):
@@ -325,12 +364,33 @@ class Forward:
         y = self.y.data_ptr()
         k("attn_plan", lambda: L.hm_attention_plan(q_len.data_ptr(), n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads,
                                                    self.attn_work.data_ptr(), st))
+        tp = self.tp
+        if tp is not None and self.residual_in_gemm:
+            raise ValueError("tensor parallelism needs the O / down partials in fp32 buffers (residual_in_gemm off)")
+
+        def norm(yb, wt):
+            # x += y (the previous O / down projection; with TP, y = both GPUs' partials), h = rmsnorm(x)
+            if tp is None:
+                k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yb, wt, M, d, cfg.eps,
+                                                           self.h.data_ptr(), mp, st))
+            else:
+                loc, peer = (None, None) if yb is None else (tp.y[yb].data_ptr(), tp.y_peer[yb].data_ptr())
+                k("rmsnorm", lambda: L.hm_rmsnorm_residual2(self.x.data_ptr(), loc, peer, wt, M, d, cfg.eps,
+                                                            self.h.data_ptr(), mp, st))
+
+        def y_out(b):   # where the O (b = 0) / down (b = 1) projection writes its fp32 (partial) output
+            return y if tp is None else tp.y[b].data_ptr()
+
+        def allreduce_sync():
+            if tp is not None:
+                k("tp_barrier", lambda: tp.barrier(s_obj) or 0)
+
         for li, layer in enumerate(w.layers):
             kc, vc = self.cache.k(li).data_ptr(), self.cache.v(li).data_ptr()
-            # x += y (previous down-proj; none before layer 0), h = rmsnorm(x)
-            yp = None if (li == 0 or self.residual_in_gemm) else y
-            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yp, layer["ln1"].data_ptr(), M, d,
-                                                       cfg.eps, self.h.data_ptr(), mp, st))
+            if li == 0 or self.residual_in_gemm:
+                norm(None, layer["ln1"].data_ptr())
+            else:
+                norm(y if tp is None else 1, layer["ln1"].data_ptr())
             if self.fused_qkv_rope:   # QKV projection, RoPE and the KV append in one kernel (same bits)
                 k("gemm_qkv", lambda: L.hm_gemm_qkv_rope(
                     self.h.data_ptr(), d, layer["wqkv"].data_ptr(), d, M, d, layer["bqkv"].data_ptr(), cfg.n_heads,
@@ -351,18 +411,20 @@ class Forward:
                                                   cfg.n_kv_heads, cfg.head_dim, self.cache.max_len, self.scale,
                                                   self.attn.data_ptr(), self.attn_work.data_ptr(), 1,
                                                   self.cache.n_slots, M, st))
-            epi_r, y_r, y_n = (EPI_RESIDUAL, self.x.data_ptr(), None) if self.residual_in_gemm else (EPI_F32, y, y)
+            epi_r = EPI_RESIDUAL if self.residual_in_gemm else EPI_F32
+            y_o = self.x.data_ptr() if self.residual_in_gemm else y_out(0)
             k("gemm_o", lambda: L.hm_gemm(epi_r, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
-                                          M, d, hd_all, None, None, 0, y_r, d, None, None, mp, st))
-            k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), y_n, layer["ln2"].data_ptr(), M, d,
-                                                       cfg.eps, self.h.data_ptr(), mp, st))
+                                          M, d, hd_all, None, None, 0, y_o, d, None, None, mp, st))
+            allreduce_sync()
+            norm(None if self.residual_in_gemm else (y if tp is None else 0), layer["ln2"].data_ptr())
             k("gemm_gate_up", lambda: L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M,
                                                 2 * cfg.ffn, d, None, self.act.data_ptr(), cfg.ffn, None, 0, None,
                                                 None, mp, st))
+            y_d = self.x.data_ptr() if self.residual_in_gemm else y_out(1)
             k("gemm_down", lambda: L.hm_gemm(epi_r, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
-                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y_r, d, None, None, mp, st))
-        k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), None if self.residual_in_gemm else y,
-                                                   w.final_ln.data_ptr(), M, d, cfg.eps, self.h.data_ptr(), mp, st))
+                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y_d, d, None, None, mp, st))
+            allreduce_sync()
+        norm(None if self.residual_in_gemm else (y if tp is None else 1), w.final_ln.data_ptr())
         if logits_out is not None:
             check(L.hm_gemm(EPI_STORE, self.h.data_ptr(), d, w.lm_head.data_ptr(), d, M, cfg.vocab, d, None,
                             logits_out.data_ptr(), cfg.vocab, None, 0, None, None, mp, st))
