@@ -620,7 +620,7 @@ def run_rollout(args, dist, pk):
                 "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": None,
                 "per_launch_flops": 2.0 * M * N_ * K_, "M": M, "N": N_, "K": K_}
     else:   # attention: KV bytes
-        kvb = float((P + T // 2 + q_lens).sum()) * cfg.n_kv_heads * cfg.head_dim * 2 * 2 * k_n
+        kvb = float((P + T // 2 + q_lens).sum()) * w.cfg.n_kv_heads * w.cfg.head_dim * 2 * 2 * k_n
         ach = kvb / (k_ms / 1e3) / 1e9
         roof = {"kernel": label, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "traffic": None}

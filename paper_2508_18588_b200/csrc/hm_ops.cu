@@ -195,8 +195,11 @@ __global__ void k_tp_barrier(int* my_flag, int* peer_flag, int* gen) {
   __threadfence_system();
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(peer_flag), "r"(g) : "memory");
   int v;
+  const long long t0 = clock64();
   do {
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(my_flag) : "memory");
+    // a peer that never arrives (diverged control flow) fails the launch loudly instead of hanging the GPU
+    if (v < g && clock64() - t0 > (30ll << 30)) __trap();
   } while (v < g);
   __threadfence_system();
 }

@@ -380,7 +380,8 @@ class RolloutEngine:
                 if done:
                     start_harvest(done)
                 if on_check is not None and busy:
-                    live = {ln: busy[ln].key for ln in busy if ln in was_busy and gl[ln] < tl[ln]}
+                    # lanes still running the request the snapshot saw (a refilled lane's gen_len is stale)
+                    live = {ln: busy[ln].key for ln in busy if was_busy.get(ln) is busy[ln] and gl[ln] < tl[ln]}
                     ev_l = [ln for ln in (on_check(live, gl, it_host, len(queue)) or []) if ln in live]
                     if ev_l:
                         evict(ev_l)

@@ -370,9 +370,9 @@ class Forward:
 
         def norm(yb, wt):
             # x += y (the previous O / down projection; with TP, y = both GPUs' partials), h = rmsnorm(x)
-            if tp is None:
-                k("rmsnorm", lambda: L.hm_rmsnorm_residual(self.x.data_ptr(), yb, wt, M, d, cfg.eps,
-                                                           self.h.data_ptr(), mp, st))
+            if tp is None:   # (hm_rmsnorm_residual2 without a second partial: the d <= 4096 kernel or any-d one)
+                k("rmsnorm", lambda: L.hm_rmsnorm_residual2(self.x.data_ptr(), yb, None, wt, M, d, cfg.eps,
+                                                            self.h.data_ptr(), mp, st))
             else:
                 loc, peer = (None, None) if yb is None else (tp.y[yb].data_ptr(), tp.y_peer[yb].data_ptr())
                 k("rmsnorm", lambda: L.hm_rmsnorm_residual2(self.x.data_ptr(), loc, peer, wt, M, d, cfg.eps,
