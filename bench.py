@@ -379,7 +379,8 @@ def cpu_rollout_sample(cfg, seed, prompts, T, s, G, threads, W=None):
     torch.set_num_threads(threads)
     if W is None:
         from paper_2508_18588_b200.model import Weights
-        w = Weights(cfg, "cuda", seed=seed)
+        # generated on the host: the reference arm never touches the GPU (same seed, CPU RNG stream)
+        w = Weights(cfg, "cpu", seed=seed)
         W = R.weights_fp32(w, "cpu")
         del w
     eng = R.CpuRollout(cfg, W, prompts.shape[1] + T + 40)
@@ -974,6 +975,121 @@ def run_longtail(args, dist, pk):
     return line, {"cfg": cfg}
 
 
+# ------------------------------------------------------------------ BASELINE.md section 4 CPU plan
+
+def _ref_replay_shard(args):
+    """One worker of the pool: the reference's build_tree + replay_response over a shard of prompts."""
+    ref_path, items = args
+    import sys as _sys
+    if ref_path not in _sys.path:
+        _sys.path.insert(0, ref_path)
+    from rhymesim.history import Response, build_tree
+    from rhymesim.spec_engine import SpecConfig, SpecStats, replay_response
+    t_build = t_replay = 0.0
+    st = SpecStats()
+    tpis = []
+    for pid, hist, truths in items:
+        t0 = time.perf_counter()
+        tree = build_tree(pid, 1, [Response(pid, 1, [int(x) for x in tok], float(r)) for tok, r in hist])
+        t1 = time.perf_counter()
+        for tr in truths:
+            rr = replay_response([int(x) for x in tr], tree, SpecConfig(), stats=st)
+            tpis.append(list(rr.tokens_per_iter))
+        t_build += t1 - t0
+        t_replay += time.perf_counter() - t1
+    stats = np.array([st.tokens_total, st.tokens_speculated, st.tokens_accepted, st.verify_passes, st.decode_passes],
+                     np.int64)
+    return t_build, t_replay, stats, tpis
+
+
+def run_cpu_plan(args, dist, pk):
+    """(1) the reference's own HistoSpec bookkeeping (rhymesim build_tree +
+    replay_response, from baseline/_ref) on the host cores, single process and a process pool, checked
+    bit-exact against the GPU replay of the same inputs; (2) configs[0] end to end on CPU (tiny model, fp32
+    torch on all threads, oracle drafting) beside the same workload on the GPU engine."""
+    import multiprocessing as mproc
+    import subprocess as sp
+    import torch
+    from paper_2508_18588_b200.engine import RolloutEngine
+    from paper_2508_18588_b200.index import GpuIndex
+    from paper_2508_18588_b200.model import TINY, Weights
+    from paper_2508_18588_b200.spec_engine import SpecConfig, replay_batch
+    from paper_2508_18588_b200.workload import ReplayWorkload, history_lists
+    cores = os.cpu_count() or 1
+    try:
+        model = [l.split(":", 1)[1].strip() for l in sp.run(["lscpu"], capture_output=True, text=True).stdout
+                 .splitlines() if l.startswith("Model name")][0]
+    except Exception:   # noqa: BLE001
+        model = "unknown"
+    out = {"impl": "cpu-plan", "host": {"cpu_count": cores, "lscpu_model": model}}
+    # ---- (1) bookkeeping: configs[1]-shaped prompts (8 x 4096-token (D) histories at s, 8 truths each)
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    data = ReplayWorkload(prompts=args.ref_prompts, samples=args.samples, length=args.length,
+                          similarity=args.similarity, seed=args.seed).generate()
+    hists = history_lists(data)
+    S = args.samples
+    items = [("p%d" % p, [(h, r) for h, r in hists[p]], [data["truths"][p * S + j] for j in range(S)])
+             for p in range(len(hists))]
+    n_tok = int(sum(len(t) for _, _, ts in items for t in ts))
+    if os.path.isfile(os.path.join(ref, "rhymesim", "history.py")):
+        t0 = time.perf_counter()
+        tb, tr, st1, tpi1 = _ref_replay_shard((ref, items))
+        single = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        shards = [(ref, items[i::cores]) for i in range(min(cores, len(items)))]
+        with mproc.get_context("spawn").Pool(len(shards)) as pool:
+            parts = pool.map(_ref_replay_shard, shards)
+        pooled = time.perf_counter() - t0
+        # GPU replay of the same inputs: bit-exact tokens_per_iter and stats (the parity half of the plan)
+        idx = GpuIndex([[(h, r) for h, r in hists[p]] for p in range(len(hists))])
+        per, st_gpu = replay_batch(idx, [p for p in range(len(hists)) for _ in range(S)],
+                                   [t for _, _, ts in items for t in ts], SpecConfig())
+        out["bookkeeping"] = {
+            "kind": "reference", "source": "rhymesim (baseline/_ref) build_tree + replay_response",
+            "sample": "%d prompts x %d truths x %d tokens, G=8 (D) histories s=%.2f" % (
+                len(items), S, args.length, args.similarity),
+            "single_process_tokens_per_s": n_tok / single, "single_build_s": tb, "single_replay_s": tr,
+            "pool_tokens_per_s": n_tok / pooled, "pool_workers": len(shards),
+            "accepted_per_verify": float(st1[2] / max(st1[3], 1)),
+            "gpu_bit_exact": bool(per == tpi1 and (st_gpu.sum(axis=0) == st1).all())}
+    else:
+        out["bookkeeping"] = {"unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}
+    # ---- (2) configs[0] end to end: tiny decoder, 64 prompts x 2 epochs (epoch 2 HistoSpec, (D) s = 0.7)
+    from oracle import model_ref as R
+    torch.set_num_threads(cores)
+    n_p, P0, T0 = 64, 32, args.tiny_tokens
+    prompts = np.random.default_rng([args.seed, 5]).integers(0, TINY.vocab, size=(n_p, P0), dtype=np.int32)
+    Wc = R.weights_fp32(Weights(TINY, "cpu", seed=args.seed), "cpu")
+    eng_c = R.CpuRollout(TINY, Wc, P0 + T0 + 40)
+    base_c, pre0, dec0, _, _, _ = eng_c.rollout([list(p) for p in prompts], T0, None)
+    rng = np.random.default_rng([args.seed, 6])
+    toks, rew = derived_history(rng, np.asarray(base_c, dtype=np.int32), 0.7, 8, TINY.vocab)
+    hc = [[(toks[p, g], float(rew[p, g])) for g in range(8)] for p in range(n_p)]
+    out_c, pre1, dec1, it1, acc1, ver1 = eng_c.rollout([list(p) for p in prompts], T0, hc)
+    n_gen = n_p * T0
+    dev = torch.device("cuda", dist.local)
+    wg = Weights(TINY, dev, seed=args.seed)
+    eng = RolloutEngine(TINY, wg, n_slots=n_p, max_len=P0 + T0 + 8, device=dev)
+    b0 = eng.rollout(prompts, [T0] * n_p, speculate=False)
+    toks_g, rew_g = derived_history(np.random.default_rng([args.seed, 6]), b0.tokens, 0.7, 8, TINY.vocab)
+    idx_g = GpuIndex([[(toks_g[p, g], float(rew_g[p, g])) for g in range(8)] for p in range(n_p)])
+    b1 = eng.rollout(prompts, [T0] * n_p, slots=np.arange(n_p), index=idx_g, speculate=True)
+    out["configs0"] = {
+        "workload": "configs[0]: tiny 2-layer decoder (d 256, vocab 4096), %d prompts x 2 epochs, %d-token "
+                    "greedy rollouts, epoch-2 HistoSpec with (D) s=0.7 G=8 history" % (n_p, T0),
+        "cpu": {"kind": "port", "cores": cores, "epoch1_nonspec_tokens_per_s": n_gen / (pre0 + dec0),
+                "epoch2_histospec_tokens_per_s": n_gen / (pre1 + dec1),
+                "accepted_per_verify": acc1 / max(ver1, 1), "spec_equals_greedy": out_c == base_c,
+                "note": "fp32 torch on all host threads, drafting by the C restatement of extract_draft "
+                        "(pinned to the reference's golden vectors)"},
+        "gpu": {"epoch1_nonspec_tokens_per_s": n_gen / (b0.gpu_ms / 1e3),
+                "epoch2_histospec_tokens_per_s": n_gen / (b1.gpu_ms / 1e3),
+                "spec_equals_greedy": bool(np.array_equal(b0.tokens, b1.tokens)),
+                "note": "bf16 engine on one B200 (different arithmetic from the fp32 CPU model: outputs "
+                        "are compared within each engine)"}}
+    return out
+
+
 # ------------------------------------------------------------------ lookup microbenchmark
 
 def run_lookup(args, dist, pk):
@@ -1142,7 +1258,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="rollout", choices=["rollout", "replay", "lookup", "similarity",
-                                                                  "longtail"])
+                                                                  "longtail", "cpu-plan"])
     ap.add_argument("--model", default="qwen2.5-1.5b-shape")
     ap.add_argument("--batch", type=int, default=1024, help="resident sequences per wave (rollout)")
     ap.add_argument("--prompt-len", type=int, default=256)
@@ -1164,6 +1280,7 @@ def main():
     ap.add_argument("--compare-waves", action="store_true", help="longtail: also time static waves")
     ap.add_argument("--kv-gb", type=float, default=120.0, help="longtail: KV-cache budget per GPU (GB)")
     ap.add_argument("--tp", type=int, default=1, choices=[1, 2], help="rollout: tensor-parallel GPUs per worker")
+    ap.add_argument("--tiny-tokens", type=int, default=300, help="cpu-plan: configs[0] response length")
     ap.add_argument("--migrate", action="store_true", help="longtail: intra-step straggler migration")
     ap.add_argument("--alpha-pct", type=float, default=10.0, help="longtail: migration alpha (percent)")
     ap.add_argument("--growth-sigma", type=float, default=0.25, help="longtail: epoch length-growth noise")
@@ -1195,6 +1312,10 @@ def main():
         line, data = run_similarity(args, dist, pk)
     elif args.workload == "longtail":
         line, data = run_longtail(args, dist, pk)
+    elif args.workload == "cpu-plan":
+        print(json.dumps(run_cpu_plan(args, dist, pk)), flush=True)
+        dist.close()
+        return
     else:
         line, data = run_lookup(args, dist, pk)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
