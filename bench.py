@@ -736,8 +736,14 @@ def run_longtail(args, dist, pk):
     n_prompts = args.prompts * world                       # weak scaling: args.prompts per GPU
     rng = np.random.default_rng([args.seed, 4242])
     z = rng.standard_normal(n_prompts)
+    # last epoch: per-prompt median and per-sample lengths (HistoPipe ranks on these); this epoch every prompt's
+    # lengths grow by a per-prompt factor exp(growth_sigma z') (0 without --migrate: lengths repeat), so some
+    # rollouts outgrow beta x their group's longest history -- the stragglers migration_decision moves
     med = np.clip(np.exp(np.log(args.len_median) + args.len_sigma * z), lo, hi)
-    tgt = np.clip(np.rint(med[:, None] * np.exp(0.08 * rng.standard_normal((n_prompts, S)))), lo, hi).astype(int)
+    tgt_last = np.clip(np.rint(med[:, None] * np.exp(0.08 * rng.standard_normal((n_prompts, S)))), lo, hi)
+    g_sigma = args.growth_sigma if args.migrate else 0.0
+    growth = np.exp(g_sigma * np.random.default_rng([args.seed, 4343]).standard_normal(n_prompts))
+    tgt = np.clip(np.rint(tgt_last * growth[:, None]), lo, hi).astype(int)
     w = Weights(cfg, dev, seed=args.seed)
 
     def make_engine(max_target):
@@ -788,9 +794,8 @@ def run_longtail(args, dist, pk):
     migrate = bool(args.migrate and world > 1)
     # last epoch's lengths: this epoch's targets over a per-rollout growth factor; stragglers that outgrow
     # beta x their group's longest history are the rollouts HistoPipe migrates (scheduler.py:304-330)
-    grow = np.exp(args.growth_sigma * np.random.default_rng([args.seed, 4343]).standard_normal(tgt.shape))
-    hist_len = np.clip(tgt / grow, lo, hi)
-    policy = W.MigrationPolicy(alpha_pct=args.alpha_pct, beta=W.beta_from_history(list(grow.ravel())))
+    hist_len = tgt_last
+    policy = W.MigrationPolicy(alpha_pct=args.alpha_pct, beta=W.beta_from_history(list(growth)))
     run_no = [0]
     mig_log = {"evicted": 0, "received": 0}
 
@@ -818,6 +823,8 @@ def run_longtail(args, dist, pk):
                     act[group_of_rank[r]] = act.get(group_of_rank[r], 0.0) + ld
             out = []
             for ln, k in live.items():
+                if k in moved_in:     # a rollout migrates at most once
+                    continue
                 kind, tg = W.migration_decision(g_me, max_hist, int(gl[ln]), total - remaining, total, policy,
                                                 len(groups), act)
                 if kind == "intra_step" and tg is not None:
@@ -834,10 +841,14 @@ def run_longtail(args, dist, pk):
             # a migrated-in rollout continues without drafts: its history slot indexes the source GPU's
             # GpuIndex (the receiving engine's graph holds this rank's index)
             got = [dataclasses.replace(r, slot=-1) for r in broker.poll()]
+            for r in got:
+                queue_t[r.key] = r.target_len
+                moved_in.add(r.key)
             mig_log["received"] += len(got)
             return got
 
         dest = {}
+        moved_in = set()
         res_ = eng.rollout_stream(queue, index=idx_, speculate=spec_on, on_check=on_check, on_evict=on_evict,
                                   inbox=inbox, keep_alive=broker.keep_alive, max_target=hi)
         dist.barrier()
@@ -963,7 +974,8 @@ def run_longtail(args, dist, pk):
         "migration": {"enabled": migrate, "alpha_pct": args.alpha_pct, "beta": policy.beta,
                       "evicted_rank0": mig_log["evicted"], "received_rank0": mig_log["received"],
                       "note": "intra-step straggler migration (scheduler.py:304-330) with KV recompute by prefill "
-                              "on the receiving GPU; history lengths = targets / exp(%.2f z)" % args.growth_sigma},
+                              "on the receiving GPU; this epoch's lengths = last epoch's x exp(%.2f z) per "
+                              "prompt, beta = beta_from_history(growth rates)" % g_sigma},
         "static_waves_value": (dist.sum(n_tok) / dist.max(waves_ms / 1e3)) if waves_ms else None,
         "occupancy": row["occupancy"],
         "nonspec_value": nonspec,
