@@ -452,8 +452,10 @@ def run_rollout(args, dist, pk):
             torch.cuda.synchronize()
             bcast_ms = 1e3 * (time.perf_counter() - t0)
         bcast_gbps = w.flat.numel() * 2 / (bcast_ms / 1e3) / 1e9
+    from paper_2508_18588_b200.spec_engine import SpecConfig
+    spec_cfg = SpecConfig(window_max=args.window_max)   # the reference's defaults unless --window-max
     eng = RolloutEngine(w.cfg, w, n_slots=B, max_len=P + T, device=dev, attention=args.attention,
-                        temperature=args.temperature, seed=args.seed, tp_group=tp_group)
+                        temperature=args.temperature, seed=args.seed, tp_group=tp_group, spec=spec_cfg)
 
     def prompt_tokens(pid):
         return np.random.default_rng([args.seed, 1000 + pid]).integers(0, cfg.vocab, size=P, dtype=np.int32)
@@ -646,7 +648,8 @@ def run_rollout(args, dist, pk):
         "value": value, "unit": "tokens/s", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": e2e_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts (sample-id token per sample), random-init weights (seed %d), (%s) history "
-                "s=%.2f G=%d per sequence" % (args.seed, args.history, args.similarity, G),
+                "s=%.2f G=%d per sequence, SpecConfig window_max %d" % (args.seed, args.history, args.similarity, G,
+                                                                        args.window_max),
         "config": {"workload": "configs[%d]: %s, %d prompts x %d samples per wave (%d resident sequences), "
                                "%d-token prompts, %d-token %s rollouts, waves cycle over %d prompts per GPU" % (
                                    2 if sampling else 1, cfg.name, per_wave, S, B, P, T,
@@ -1293,6 +1296,7 @@ def main():
     ap.add_argument("--kv-gb", type=float, default=120.0, help="longtail: KV-cache budget per GPU (GB)")
     ap.add_argument("--tp", type=int, default=1, choices=[1, 2], help="rollout: tensor-parallel GPUs per worker")
     ap.add_argument("--tiny-tokens", type=int, default=300, help="cpu-plan: configs[0] response length")
+    ap.add_argument("--window-max", type=int, default=32, help="rollout: SpecConfig.window_max (reference default 32)")
     ap.add_argument("--migrate", action="store_true", help="longtail: intra-step straggler migration")
     ap.add_argument("--alpha-pct", type=float, default=10.0, help="longtail: migration alpha (percent)")
     ap.add_argument("--growth-sigma", type=float, default=0.25, help="longtail: epoch length-growth noise")
