@@ -863,10 +863,11 @@ def run_longtail(args, dist, pk):
     if migrate:   # rollouts that finished on another rank come home (host exchange of the few migrated ones)
         import torch.distributed as tdist
         gathered = [None] * world
-        tdist.all_gather_object(gathered, {k: v for k, v in base.tokens.items() if k not in queue_t})
+        own = set(keys)
+        tdist.all_gather_object(gathered, {k: v for k, v in base.tokens.items() if k not in own})
         for part in gathered:
             for k, v in part.items():
-                if k in queue_t:
+                if k in own:
                     base.tokens[k] = v
     n_tok = int(sum(targets))
     truth = np.concatenate([base.tokens[k] for k in keys]).astype(np.int32)
