@@ -187,6 +187,17 @@ int hs_similarity_replay_isa(const HsIndexView* view, const int32_t* d_isa, int3
                              const int32_t* d_tokens, const int64_t* d_resp_off, const int32_t* d_slot_of_resp,
                              int32_t prefix_len, int64_t* d_accepted, hs_stream_t stream);
 
+/* Candidate branches of a draft tree (north_star (1) "frequency-weighted candidate branches"): for query i,
+ * up to `width` (<= 8) branches, each a first token below the matched prefix -- the node's token children
+ * ranked by reward mass, ties to the smaller token (history.py:322-331 order) -- followed by that child's greedy
+ * (heavy) continuation, `window` tokens in all.  Branch 0 equals extract_draft's draft (history.py:302-333).
+ * Out: d_out_tok [n, width, out_stride], d_out_len [n, width], d_out_mass [n, width] (fixed-point mass of the
+ * branch's first token).  Unused branches have length 0. */
+int hs_lookup_branches(const HsIndexView* view, int32_t n, const int32_t* d_slot, const int32_t* d_prefix,
+                       int32_t prefix_stride, const int32_t* d_prefix_len, const int32_t* d_window, int32_t width,
+                       int32_t* d_out_tok, int32_t out_stride, int32_t* d_out_len, int64_t* d_out_mass,
+                       hs_stream_t stream);
+
 /* Continuous batching (engine lanes): lane d_lane[i] takes a new sequence whose
  * generated tokens so far are d_tok[d_tok_off[i] : d_tok_off[i+1]] (empty for a fresh prompt; a migrated
  * rollout's prefix, whose KV the admission prefill recomputed) followed by d_argmax[d_first_row[i]] when

@@ -80,6 +80,24 @@ def extract_draft(corpus, prefix, window):
     return out, len(prefix), mass0
 
 
+def draft_branches(corpus, prefix, window, width):
+    """Candidate branches of a draft tree, brute force: the token children below `prefix` ranked by
+    (mass desc, token asc) -- the order extract_draft takes its first token in (history.py:322-331) -- each
+    followed by extract_draft's greedy continuation from prefix + [token].  Branch 0 == extract_draft."""
+    live = occurrences(corpus, list(prefix))
+    masses = {}
+    for r, p in live:
+        toks = corpus[r][0]
+        if p < len(toks):
+            masses[toks[p]] = masses.get(toks[p], 0.0) + corpus[r][1]
+    ranked = sorted(masses, key=lambda t: (-masses[t], t))[:width]
+    out = []
+    for t in ranked:
+        cont = extract_draft(corpus, list(prefix) + [t], window - 1)[0] if window > 1 else []
+        out.append([t] + cont)
+    return out, [masses[t] for t in ranked]
+
+
 # -- spec engine state machine (spec_engine.py) ------------------------------
 
 

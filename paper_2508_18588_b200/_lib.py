@@ -66,6 +66,7 @@ SIGNATURES = {
     "hs_index_inverse_sa": [ctypes.POINTER(HsIndexView), _P, _P],
     "hs_similarity_replay_isa": [ctypes.POINTER(HsIndexView), _P, _I32, _P, _P, _P, _I32, _P, _P],
     "hs_pack_rows": [_P, _I64, _P, _P, _P, _I32, _P, _P],
+    "hs_lookup_branches": [ctypes.POINTER(HsIndexView), _I32, _P, _P, _I32, _P, _P, _I32, _P, _I32, _P, _P, _P],
     "hs_lane_admit": [_I32] + [_P] * 13 + [_P, _I32] + [_P] * 13,
     "hs_mutate_bursts": [_P, _P, _I32, _I32, ctypes.c_double, ctypes.c_double, _I32, ctypes.c_uint64, _P, _P, _P],
 }

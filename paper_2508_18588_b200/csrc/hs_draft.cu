@@ -712,6 +712,139 @@ __global__ void k_similarity_replay_isa(HsIndexView V, const int32_t* __restrict
 
 using namespace hs;
 
+// Candidate branches of a draft tree (north_star (1): frequency-weighted candidate branches): the children of
+// the node the prefix matches, ranked by reward mass (ties to the smaller token -- the order extract_draft
+// picks its first token in, history.py:322-331), each followed by its own greedy (heavy) continuation.
+// Branch 0 is exactly the reference draft; branches 1..W-1 are the runner-up first tokens.  A prefix that
+// ends inside an edge (one continuation) or in a leaf has one branch.  One warp per query:
+//   [first, last) = the prefix's SA interval (binary search); locus depth < m... == m -> at a node: child
+//   boundaries are the k in (first, last) with lcp[k] == m; a child's mass is a wsum difference, its token
+//   text[sa[a] + m] (a terminal child is not a token child); its heavy end is heavy[] at the child's own
+//   first minimum-LCP boundary (or its only suffix).
+__global__ void k_lookup_branches(HsIndexView V, int32_t n, const int32_t* __restrict__ slot,
+                                  const int32_t* __restrict__ prefix, int32_t prefix_stride,
+                                  const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ window,
+                                  int32_t width, int32_t* __restrict__ out_tok, int32_t out_stride,
+                                  int32_t* __restrict__ out_len, int64_t* __restrict__ out_mass) {
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= n) return;
+  const int lane = lane_id();
+  const int32_t s = slot[w], m = prefix_len[w], win = window[w];
+  const int32_t* pre = prefix + (int64_t)w * prefix_stride;
+  int32_t* lens = out_len + (int64_t)w * width;
+  int64_t* masses = out_mass + (int64_t)w * width;
+  for (int b = lane; b < width; b += 32) { lens[b] = 0; masses[b] = 0; }
+  __syncwarp();
+  if (s < 0 || s >= V.n_slots || m < 1 || win < 1) return;
+  const int64_t S = V.slot_sa_off[s], E = V.slot_sa_off[s + 1];
+  int64_t lo = S, hi = E;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cmp_suffix(V.text, V.sa[mid], pre, m) < 0) lo = mid + 1; else hi = mid;
+  }
+  const int64_t first = lo;
+  hi = E;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (cmp_suffix(V.text, V.sa[mid], pre, m) <= 0) lo = mid + 1; else hi = mid;
+  }
+  const int64_t last = lo;
+  if (first == last) return;
+  // minimum LCP (first position) inside a range: the node owning [a, b)
+  auto min_lcp = [&](int64_t a, int64_t b, int32_t& best, int64_t& bidx) {
+    best = 0x7fffffff;
+    bidx = -1;
+    for (int64_t k = a + 1 + lane; k < b; k += 32) {
+      const int32_t v = V.lcp[k];
+      if (v < best) { best = v; bidx = k; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const int32_t ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ov < best || (ov == best && oi >= 0 && (bidx < 0 || oi < bidx))) { best = ov; bidx = oi; }
+    }
+  };
+  // top-W children (mass desc, token asc), kept identically in every lane
+  constexpr int WMAX = 8;
+  int64_t tm[WMAX];
+  int32_t tt[WMAX];
+  int64_t ta[WMAX], tb[WMAX];
+  int cnt = 0;
+  auto offer = [&](int64_t mass, int32_t tok, int64_t a, int64_t b) {
+    int pos = cnt;
+    while (pos > 0 && (mass > tm[pos - 1] || (mass == tm[pos - 1] && tok < tt[pos - 1]))) --pos;
+    if (pos >= width) return;
+    const int end = cnt < width ? cnt : width - 1;
+    for (int j = end; j > pos; --j) { tm[j] = tm[j - 1]; tt[j] = tt[j - 1]; ta[j] = ta[j - 1]; tb[j] = tb[j - 1]; }
+    tm[pos] = mass; tt[pos] = tok; ta[pos] = a; tb[pos] = b;
+    if (cnt < width) ++cnt;
+  };
+  int32_t depth = m + 1;
+  int64_t node_k = -1;
+  if (last - first > 1) min_lcp(first, last, depth, node_k);
+  if (last - first == 1 || depth > m) {
+    // a leaf or inside an edge: the single continuation (the reference draft)
+    const int32_t p = last - first == 1 ? V.sa[first] : V.heavy[node_k];
+    const int32_t t = V.text[p + m];
+    if (t >= 0) offer(V.wsum[last] - V.wsum[first], t, first, last);
+  } else {
+    // at a node: walk the child boundaries (lcp == m) in SA order
+    int64_t a = first;
+    for (int64_t base = first + 1; base <= last; base += 32) {
+      const int64_t k = base + lane;
+      const bool bnd = k < last && V.lcp[k] == m;
+      unsigned bal = __ballot_sync(0xffffffffu, bnd);
+      if (base + 31 >= last) bal |= 1u << (int)(last - base < 31 ? last - base : 31);   // the interval end
+      while (bal) {
+        const int j = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int64_t b = base + j;
+        if (b > last) break;
+        const int32_t t = V.text[V.sa[a] + m];
+        if (t >= 0) offer(V.wsum[b] - V.wsum[a], t, a, b);
+        a = b;
+        if (b == last) break;
+      }
+    }
+  }
+  // branches: each winner's heavy continuation
+  for (int c = 0; c < cnt; ++c) {
+    int32_t p;
+    if (tb[c] - ta[c] == 1) {
+      p = V.sa[ta[c]];
+    } else {
+      int32_t d2;
+      int64_t k2;
+      min_lcp(ta[c], tb[c], d2, k2);
+      p = V.heavy[k2];
+    }
+    const int32_t len = read_draft(V.text, p + m, win, out_tok + ((int64_t)w * width + c) * out_stride);
+    if (lane == 0) {
+      lens[c] = len;
+      masses[c] = tm[c];
+    }
+  }
+}
+
+extern "C" int hs_lookup_branches(const HsIndexView* view, int32_t n, const int32_t* d_slot, const int32_t* d_prefix,
+                                  int32_t prefix_stride, const int32_t* d_prefix_len, const int32_t* d_window,
+                                  int32_t width, int32_t* d_out_tok, int32_t out_stride, int32_t* d_out_len,
+                                  int64_t* d_out_mass, hs_stream_t stream) {
+  if (n < 0 || width < 1 || width > 8 || out_stride < 1) {
+    hs_set_error("hs_lookup_branches: n >= 0, 1 <= width <= 8, out_stride >= 1");
+    return HS_ERR_INVALID;
+  }
+  if (n == 0) return HS_OK;
+  hs_count_launches(1);
+  const int threads = 256;
+  const int64_t blocks = ((int64_t)n * 32 + threads - 1) / threads;
+  k_lookup_branches<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(*view, n, d_slot, d_prefix, prefix_stride,
+                                                                          d_prefix_len, d_window, width, d_out_tok,
+                                                                          out_stride, d_out_len, d_out_mass);
+  HS_CUDA_TRY(cudaGetLastError());
+  return HS_OK;
+}
+
 extern "C" int hs_lookup_batch(const HsIndexView* view, int32_t n, const int32_t* d_slot, const int32_t* d_prefix,
                                int32_t prefix_stride, const int32_t* d_prefix_len, const int32_t* d_window,
                                int32_t* d_out_tok, int32_t out_stride, int64_t* d_out_info, int32_t use_table,

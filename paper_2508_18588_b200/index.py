@@ -181,3 +181,43 @@ class GpuIndex:
             info = d_info.cpu().numpy()
         drafts = [out[i, :info[i, 1]].tolist() for i in range(n)]
         return drafts, info
+
+    def lookup_branches(self, slots, prefixes, windows, width: int = 4, stream=None):
+        """Draft-tree candidate branches per query (hs_lookup_branches): a list of up to `width` drafts per query
+        (branch 0 = extract_draft's draft, then the runner-up first tokens with their greedy continuations)
+        and their first-token masses in reward fixed point."""
+        torch = _lib.require_cuda()
+        n = len(prefixes)
+        if n == 0:
+            return [], []
+        stride = max(1, max(len(p) for p in prefixes))
+        pre = np.zeros((n, stride), dtype=np.int32)
+        plen = np.zeros(n, dtype=np.int32)
+        for i, p in enumerate(prefixes):
+            if len(p) == 0:
+                raise ValueError("prefix must be non-empty")
+            pre[i, :len(p)] = p
+            plen[i] = len(p)
+        win = np.asarray(windows, dtype=np.int32)
+        if (win < 1).any():
+            raise ValueError("window must be >= 1")
+        ostride = int(win.max())
+        dev = self.device
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev), torch.cuda.stream(s):
+            d_slot = torch.as_tensor(np.asarray(slots, dtype=np.int32)).to(dev)
+            d_pre = torch.from_numpy(pre).to(dev)
+            d_plen = torch.from_numpy(plen).to(dev)
+            d_win = torch.from_numpy(win).to(dev)
+            d_out = torch.zeros((n, width, ostride), dtype=torch.int32, device=dev)
+            d_len = torch.zeros((n, width), dtype=torch.int32, device=dev)
+            d_mass = torch.zeros((n, width), dtype=torch.int64, device=dev)
+            _lib.check(_lib.load().hs_lookup_branches(
+                ctypes.byref(self.view), n, d_slot.data_ptr(), d_pre.data_ptr(), stride, d_plen.data_ptr(),
+                d_win.data_ptr(), int(width), d_out.data_ptr(), ostride, d_len.data_ptr(), d_mass.data_ptr(),
+                s.cuda_stream))
+            out, lens, mass = d_out.cpu().numpy(), d_len.cpu().numpy(), d_mass.cpu().numpy()
+        branches = [[out[i, b, :lens[i, b]].tolist() for b in range(width) if lens[i, b] > 0] for i in range(n)]
+        masses = [[int(mass[i, b]) for b in range(width) if lens[i, b] > 0] for i in range(n)]
+        return branches, masses
+
