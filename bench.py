@@ -591,6 +591,14 @@ def run_rollout(args, dist, pk):
     ms_dev = float(np.mean(acc["ms"][-args.steps:]))
     ms_dev = dist.max(ms_dev)
     timed_res = acc["res"][-args.steps:]
+    route_iso_ms = None
+    if world > 1:   # the route alone, ranks aligned first (the in-step figure includes waiting for the slowest)
+        dist.barrier()
+        torch.cuda.synchronize()
+        r0 = time.perf_counter()
+        route(timed_res[-1].d_tokens, waves[(acc["n"] - 1) % n_waves]["pids"], 99)
+        torch.cuda.synchronize()
+        route_iso_ms = dist.max(1e3 * (time.perf_counter() - r0))
     st = np.sum([r.stats.sum(axis=0) for r in timed_res], axis=0)
     res = timed_res[-1]
     gen = B * T
@@ -661,9 +669,12 @@ def run_rollout(args, dist, pk):
                    "l2": "KV cache (%.0f GB) and weights stream far beyond the 126 MB L2" % (
                        eng.cache.buf.numel() * 2 / 1e9)},
         "attention_family": args.attention,
-        "collectives": {"weight_broadcast_ms": bcast_ms, "weight_broadcast_GBps": bcast_gbps, "rollout_route_ms_per_step": float(np.mean(
-            acc["route_ms"][-args.steps:])), "note": "epoch-boundary only: NCCL broadcast of the policy, "
-                                                     "all-to-all-v of finished rollouts to next-step owners"},
+        "collectives": {"weight_broadcast_ms": bcast_ms, "weight_broadcast_GBps": bcast_gbps,
+                        "rollout_route_ms_per_step": float(np.mean(acc["route_ms"][-args.steps:])),
+                        "rollout_route_ms_aligned": route_iso_ms,
+                        "note": "epoch-boundary only: NCCL broadcast of the policy, all-to-all-v of finished "
+                                "rollouts to next-step owners (per-step figure: host time incl. waiting for the "
+                                "slowest rank; aligned: one route after a barrier)"},
         "ingest_ms_per_step": float(np.mean([a.elapsed_time(b) for a, b in acc["ingest_ms"][-args.steps:]])),
         "distinct_4gram_ratio": distinct,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": int(waves[0]["h_prompts"].numel() * 4
