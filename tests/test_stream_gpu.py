@@ -87,3 +87,22 @@ def test_migration_with_kv_recompute(setup):
     for k in range(S["B"]):
         assert np.array_equal(toks[k], truths[k]), k
         assert (stats[k] == st[k]).all(), k
+
+
+def test_stream_sampling_equals_waves(setup):
+    """Rejection-sampling verify (T = 1) under continuous batching: the Gumbel noise is keyed by (sequence key,
+    position), so a sequence samples the same tokens whichever lane and admission time it gets -- outputs
+    equal the fixed-wave engine's with the same keys, with speculation on and off."""
+    from paper_2508_18588_b200.engine import RolloutEngine
+    S = setup
+    mk = lambda n: RolloutEngine(S["TINY"], S["w"], n_slots=n, max_len=S["P"] + S["Tmax"] + 8,  # noqa: E731
+                                 device="cuda", temperature=1.0, seed=11, check_every=4)
+    keys = np.arange(S["B"]) * 7 + 3
+    waves = mk(S["B"]).rollout(S["prompts"], [S["Tmax"]] * S["B"], speculate=False, seq_keys=keys)
+    reqs = _reqs(S)
+    for r, k in zip(reqs, keys):
+        r.key = int(k)
+    for spec in (False, True):
+        res = mk(9).rollout_stream(reqs, index=S["idx"] if spec else None, speculate=spec, admit_min=1)
+        for b, k in enumerate(keys):
+            assert np.array_equal(res.tokens[int(k)], waves.tokens[b, :S["tl"][b]]), (spec, b)
