@@ -246,6 +246,9 @@ class RolloutEngine:
 
         def admit(batch_reqs):
             nonlocal prefill_rows, admissions
+            for r in batch_reqs:   # requests that arrive later (inbox) are checked here too
+                if len(r.prompt) + int(r.target_len) > self.max_len or int(r.target_len) > max_t:
+                    raise ValueError(f"request {r.key}: prompt + target exceeds the engine's max_len / max_target")
             lanes = [free.pop() for _ in batch_reqs]
             keys = [int(r.key) for r in batch_reqs]
             first, rows = self._prefill_rows(batch_reqs, lanes, keys)
