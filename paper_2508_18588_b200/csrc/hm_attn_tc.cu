@@ -313,7 +313,11 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
       mbar_arrive_expect_tx(bar, half ? C::KVB / 2 : C::KVB);
 #pragma unroll
       for (int hb = 0; hb < HD / 64; ++hb)
+#ifdef HM_TC_KV_EVICT_FIRST   // A/B: the K/V stream (read once) marked evict-first in L2
+        tma_load_2d_evict_first(half ? half_map : full_map, bar, dst + hb * KS * 128, hb * 64, c.row0 + c.st * KS);
+#else
         tma_load_2d(half ? half_map : full_map, bar, dst + hb * KS * 128, hb * 64, c.row0 + c.st * KS);
+#endif
     };
     // slot free? (lane 0 polls, the warp follows)
     auto ready = [&](uint64_t* bar, uint32_t parity) {
@@ -745,7 +749,11 @@ __global__ void __launch_bounds__(320, 1) k_attn_tc(const __nv_bfloat16* __restr
                 w.y = pack2(f[2] * inv, f[3] * inv);
                 w.z = pack2(f[4] * inv, f[5] * inv);
                 w.w = pack2(f[6] * inv, f[7] * inv);
+#ifdef HM_TC_STORE_CS   // A/B: streaming (evict-first) output stores
+                __stcs(reinterpret_cast<uint4*>(dst + c2 * 64 + 8 * v), w);
+#else
                 *reinterpret_cast<uint4*>(dst + c2 * 64 + 8 * v) = w;
+#endif
               }
             }
           }
