@@ -340,8 +340,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1) k_attention2(const _
       mbar_arrive_expect_tx(&full[buf], bytes);
 #pragma unroll
       for (int h = 0; h < HD / 64; ++h) {
-        tma_load_2d(&tmK, &full[buf], &sK[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
-        tma_load_2d(&tmV, &full[buf], &sV[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
+        // K / V are read once: evict-first in L2 (same policy as the tcgen05 family)
+        tma_load_2d_evict_first(&tmK, &full[buf], &sK[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
+        tma_load_2d_evict_first(&tmV, &full[buf], &sV[(buf * KS) * CH + h * KS * 8], h * 64, row0 + st * KS);
       }
       return;
     }
