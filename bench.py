@@ -152,16 +152,16 @@ class Dist:
 
 def measured_traffic(key, applies=True):
     """Per-launch DRAM traffic (read + write bytes) of `key` from the committed ncu capture
-    (profiles/r01_traffic.json), or None when absent or when this run's workload is not the captured one."""
+    (profiles/r02_traffic.json), or None when absent or when this run's workload is not the captured one."""
     if not applies:
         return None, None
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
     try:
         with open(path) as f:
             ent = json.load(f).get(key)
     except (OSError, ValueError):
         return None, None
-    return (ent["bytes"], "ncu --set full, profiles/r01_traffic.json: " + ent["launch"]) if ent else (None, None)
+    return (ent["bytes"], "ncu --set full, profiles/r02_traffic.json: " + ent["launch"]) if ent else (None, None)
 
 
 def timed(fn, steps, warmup, dist, stream, gpu_index):
