@@ -136,6 +136,14 @@ int hm_rmsnorm_residual2(float* d_x, const float* d_y, const float* d_y2, const 
                          float eps, void* d_out, const int32_t* d_m, hm_stream_t stream);
 int hm_tp_barrier(int32_t* d_my_flag, int32_t* d_peer_flag, int32_t* d_gen, hm_stream_t stream);
 
+/* bf16 residual stream (Forward.residual = "bf16", the default): x (bf16 [M, d]) = bf16(x + y [+ y2]) with
+ * y the O / down projection stored in bf16 by its GEMM (and y2 the TP peer's partial), then out = rmsnorm(x) * w;
+ * y == NULL: norm only.  hm_embed_bf16: x rows = embedding rows (bf16, no conversion). */
+int hm_rmsnorm_residual_bf16(void* d_x, const void* d_y, const void* d_y2, const void* d_w, int32_t M, int32_t d,
+                             float eps, void* d_out, const int32_t* d_m, hm_stream_t stream);
+int hm_embed_bf16(const int32_t* d_tok, const void* d_emb, int32_t M, int32_t d, void* d_x, const int32_t* d_m,
+                  hm_stream_t stream);
+
 /* Work list for hm_attention's persistent schedule (once per forward: q_len is layer independent): the
  * per-sequence tile prefix and, for the tcgen05 family, each tile's sequence.  d_work holds
  * hm_attention_work_size(n_seq, max_q_len, H, KVH) int32 values. */

@@ -6,7 +6,7 @@ paper_2508_18588_b200/model.py runs on the sm_100a kernels -- RMSNorm (eps
 1e-6, weight * x * rsqrt(mean(x^2)+eps)), QKV with bias, rotate-half RoPE
 (theta 1e6, host float64 tables), GQA causal softmax attention, SwiGLU MLP,
 tied LM head.  `emulate_bf16=True` rounds activations to bf16 at exactly the
-points where the GPU path stores bf16 (normed inputs, qkv, rotated q/k, v,
+points where the GPU path stores bf16 (residual stream and projection outputs, normed inputs, qkv, rotated q/k, v,
 attention output, SwiGLU output) so the comparison isolates accumulation
 order; `emulate_bf16=False` is the plain fp32 reference.
 """
@@ -83,10 +83,11 @@ def forward_logits(cfg, W, tokens, emulate_bf16=True):
         s = torch.einsum("qhd,khd->hqk", q, kk) / math.sqrt(hd) + mask
         p = torch.softmax(s, dim=-1)
         o = _r(torch.einsum("hqk,khd->qhd", p, vv).reshape(T, H * hd), emulate_bf16)
-        x = x + o @ L["wo"].T
+        # the GPU path's default bf16 residual stream: projection rounded to bf16, sum rounded to bf16
+        x = _r(x + _r(o @ L["wo"].T, emulate_bf16), emulate_bf16)
         h = _r(rmsnorm(x, L["ln2"], cfg.eps), emulate_bf16)
         a = _r(torch.nn.functional.silu(h @ L["gate"].T) * (h @ L["up"].T), emulate_bf16)
-        x = x + a @ L["wd"].T
+        x = _r(x + _r(a @ L["wd"].T, emulate_bf16), emulate_bf16)
     h = _r(rmsnorm(x, W["final_ln"], cfg.eps), emulate_bf16)
     return h @ W["lm_head"].T
 

@@ -184,6 +184,100 @@ __global__ void k_rmsnorm_residual_g(float* __restrict__ x, const float* __restr
   }
 }
 
+// bf16 residual stream (the precision bf16 inference keeps it in): x = bf16(x + y [+ y2]) -- the projection
+// output y (and, under TP, the peer's partial y2, read in place over NVLink) rounded to bf16 by its GEMM --
+// then out = bf16(x * rsqrt(mean(x^2) + eps) * w).  Warp per row, lane-strided 8-element chunks held in
+// registers (MAXV = ceil(d / 256)); the reduction order is fixed per lane, so a row's bits depend only on it.
+template <int MAXV>
+__global__ void k_rmsnorm_residual_bf16(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
+                                        const __nv_bfloat16* y2, const __nv_bfloat16* __restrict__ w, int M, int d,
+                                        float eps, const int* m_dev, __nv_bfloat16* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int m = m_dev ? *m_dev : M;
+  const int nv = d / 8;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m;
+       row += gridDim.x * (blockDim.x >> 5)) {
+    uint4* xr = reinterpret_cast<uint4*>(x + (size_t)row * d);
+    const uint4* yr = y ? reinterpret_cast<const uint4*>(y + (size_t)row * d) : nullptr;
+    const uint4* y2r = y2 ? reinterpret_cast<const uint4*>(y2 + (size_t)row * d) : nullptr;
+    uint4 v[MAXV];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        uint4 a = xr[i];
+        if (yr) {
+          const uint4 b = yr[i];
+          uint4 c = make_uint4(0, 0, 0, 0);
+          if (y2r) c = y2r[i];
+          const uint32_t* pa = reinterpret_cast<const uint32_t*>(&a);
+          const uint32_t* pb = reinterpret_cast<const uint32_t*>(&b);
+          const uint32_t* pc = reinterpret_cast<const uint32_t*>(&c);
+          uint4 r;
+          uint32_t* pr = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pa[e]));
+            float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pb[e]));
+            if (y2r) {
+              const float2 fc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pc[e]));
+              fb.x += fc.x;
+              fb.y += fc.y;
+            }
+            const __nv_bfloat162 o = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
+            pr[e] = *reinterpret_cast<const uint32_t*>(&o);
+          }
+          a = r;
+          xr[i] = a;
+        }
+        v[k] = a;
+        const uint32_t* pv = reinterpret_cast<const uint32_t*>(&a);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[e]));
+          ss += f.x * f.x;
+          ss += f.y * f.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float r = rsqrtf(ss / (float)d + eps);
+    uint4* orow = reinterpret_cast<uint4*>(out + (size_t)row * d);
+    const uint4* w4 = reinterpret_cast<const uint4*>(w);
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        const uint4 ww = w4[i];
+        const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v[k]);
+        const uint32_t* pw = reinterpret_cast<const uint32_t*>(&ww);
+        uint4 o;
+        uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[e]));
+          const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pw[e]));
+          const __nv_bfloat162 h = __floats2bfloat162_rn(f.x * r * g.x, f.y * r * g.y);
+          po[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        orow[i] = o;
+      }
+    }
+  }
+}
+
+__global__ void k_embed_bf16(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ emb, int M, int d,
+                             const int* m_dev, __nv_bfloat16* __restrict__ x) {
+  const int m = m_dev ? *m_dev : M;
+  for (int row = blockIdx.x; row < m; row += gridDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(emb + (size_t)tok[row] * d);
+    uint4* dst = reinterpret_cast<uint4*>(x + (size_t)row * d);
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
 // Two-GPU barrier over peer memory (tensor-parallel pair): bump this GPU's generation, publish it in the
 // peer's flag word (system-scope release after a system fence: every write this stream made before -- the
 // GEMM's partial in the symmetric buffer -- is visible to the peer first), then wait until the peer's
@@ -407,6 +501,39 @@ extern "C" int hm_rmsnorm_residual2(float* d_x, const float* d_y, const float* d
   hm::k_rmsnorm_residual_g<<<(M + rows - 1) / rows < 1184 ? (M + rows - 1) / rows : 1184, 32 * rows, 0,
                              (cudaStream_t)stream>>>(d_x, d_y, d_y2, (const __nv_bfloat16*)d_w, M, d, eps, d_m,
                                                      (__nv_bfloat16*)d_out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_rmsnorm_residual_bf16(void* d_x, const void* d_y, const void* d_y2, const void* d_w, int32_t M,
+                                        int32_t d, float eps, void* d_out, const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (d % 8 || d > 8192) { hm_set_error("rmsnorm_residual_bf16: d % 8 == 0 and d <= 8192"); return HM_ERR_INVALID; }
+  if (d_y2 && !d_y) { hm_set_error("rmsnorm_residual_bf16: y2 needs y"); return HM_ERR_INVALID; }
+  const int rows = 8;
+  const dim3 grid((M + rows - 1) / rows < 1184 ? (M + rows - 1) / rows : 1184), block(32 * rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* x = (__nv_bfloat16*)d_x;
+  auto* y = (const __nv_bfloat16*)d_y;
+  auto* y2 = (const __nv_bfloat16*)d_y2;
+  auto* w = (const __nv_bfloat16*)d_w;
+  auto* out = (__nv_bfloat16*)d_out;
+  const int nv = (d + 255) / 256;
+  if (nv <= 2) hm::k_rmsnorm_residual_bf16<2><<<grid, block, 0, st>>>(x, y, y2, w, M, d, eps, d_m, out);
+  else if (nv <= 4) hm::k_rmsnorm_residual_bf16<4><<<grid, block, 0, st>>>(x, y, y2, w, M, d, eps, d_m, out);
+  else if (nv <= 8) hm::k_rmsnorm_residual_bf16<8><<<grid, block, 0, st>>>(x, y, y2, w, M, d, eps, d_m, out);
+  else if (nv <= 16) hm::k_rmsnorm_residual_bf16<16><<<grid, block, 0, st>>>(x, y, y2, w, M, d, eps, d_m, out);
+  else hm::k_rmsnorm_residual_bf16<32><<<grid, block, 0, st>>>(x, y, y2, w, M, d, eps, d_m, out);
+  HM_LAUNCH_CHECK();
+  return HM_OK;
+}
+
+extern "C" int hm_embed_bf16(const int32_t* d_tok, const void* d_emb, int32_t M, int32_t d, void* d_x,
+                             const int32_t* d_m, hm_stream_t stream) {
+  if (M <= 0) return HM_OK;
+  if (d % 8) { hm_set_error("embed_bf16: d % 8 == 0"); return HM_ERR_INVALID; }
+  hm::k_embed_bf16<<<M < 4096 ? M : 4096, 128, 0, (cudaStream_t)stream>>>(d_tok, (const __nv_bfloat16*)d_emb, M, d,
+                                                                         d_m, (__nv_bfloat16*)d_x);
   HM_LAUNCH_CHECK();
   return HM_OK;
 }

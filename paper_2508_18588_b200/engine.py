@@ -73,7 +73,7 @@ class RolloutEngine:
         self.fwd.temperature, self.fwd.seed = float(temperature), int(seed)
         if tp_group is not None:
             from .tp import TensorParallel
-            self.fwd.tp = TensorParallel(tp_group, self.fwd.max_rows, cfg.d_model, self.device)
+            self.fwd.tp = TensorParallel(tp_group, self.fwd.max_rows, cfg.d_model, self.device, dtype=self.fwd.x.dtype)
         self.prefill_rows = prefill_rows
         i32 = dict(dtype=torch.int32, device=self.device)
         R = self.fwd.max_rows

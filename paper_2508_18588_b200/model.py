@@ -48,6 +48,8 @@ SIGNATURES = {
     "hm_set_gemm_pair": [_I32],
     "hm_rmsnorm_residual2": [_P, _P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
     "hm_tp_barrier": [_P, _P, _P, _P],
+    "hm_rmsnorm_residual_bf16": [_P, _P, _P, _P, _I32, _I32, _F32, _P, _P, _P],
+    "hm_embed_bf16": [_P, _P, _I32, _I32, _P, _P, _P],
     "hm_f32_gemm": [_P, _I64, _P, _I64, _I32, _I32, _I32, _P, _P, _I64, _I32, _P],
     "hm_f32_rmsnorm": [_P, _P, _I32, _I32, _F32, _P, _P],
     "hm_f32_rope_kv_append": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P],
@@ -297,14 +299,21 @@ class KVCache:
 class Forward:
     """Preallocated activations for up to max_rows verify rows; runs the forward."""
 
-    def __init__(self, w: Weights, cache: KVCache, max_rows: int, device):
+    def __init__(self, w: Weights, cache: KVCache, max_rows: int, device, residual: str | None = None):
+        """residual: "bf16" (default; HM_RESIDUAL=fp32 in the environment changes it) keeps the residual stream
+        x and the O / down projection outputs y in bf16, the precision bf16 inference keeps them in; "fp32"
+        keeps both in fp32 (round 1's layout: 2x the bytes through every norm)."""
         import torch
         cfg = w.cfg
         self.w, self.cache, self.cfg, self.max_rows, self.device = w, cache, cfg, max_rows, device
         M, d = max_rows, cfg.d_model
         bf = dict(dtype=torch.bfloat16, device=device)
-        self.x = torch.empty((M, d), dtype=torch.float32, device=device)
-        self.y = torch.empty((M, d), dtype=torch.float32, device=device)   # O/down-proj output, added in the norm
+        self.residual = residual or os.environ.get("HM_RESIDUAL", "bf16")
+        if self.residual not in ("bf16", "fp32"):
+            raise ValueError(f"residual must be 'bf16' or 'fp32', got {self.residual!r}")
+        rdt = torch.bfloat16 if self.residual == "bf16" else torch.float32
+        self.x = torch.empty((M, d), dtype=rdt, device=device)
+        self.y = torch.empty((M, d), dtype=rdt, device=device)   # O/down-proj output, added in the norm
         self.h = torch.empty((M, d), **bf)
         self.qkv = torch.empty((M, cfg.qkv_dim), **bf)
         self.q = torch.empty((M, cfg.n_heads, cfg.head_dim), **bf)   # used as [KVH][rows][G][hd] (hm_rope_kv_append)
@@ -359,7 +368,13 @@ class Forward:
             e1.record(s_obj)
             prof.append((label, e0, e1))
 
-        k("embed", lambda: L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
+        r16 = self.residual == "bf16"
+        if r16 and self.residual_in_gemm:
+            raise ValueError("residual_in_gemm is an fp32-residual option")
+        if r16:
+            k("embed", lambda: L.hm_embed_bf16(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
+        else:
+            k("embed", lambda: L.hm_embed(tokens.data_ptr(), w.embed.data_ptr(), M, d, self.x.data_ptr(), mp, st))
         hd_all = cfg.n_heads * cfg.head_dim
         y = self.y.data_ptr()
         k("attn_plan", lambda: L.hm_attention_plan(q_len.data_ptr(), n_seq, max_q_len, cfg.n_heads, cfg.n_kv_heads,
@@ -370,7 +385,14 @@ class Forward:
 
         def norm(yb, wt):
             # x += y (the previous O / down projection; with TP, y = both GPUs' partials), h = rmsnorm(x)
-            if tp is None:   # (hm_rmsnorm_residual2 without a second partial: the d <= 4096 kernel or any-d one)
+            if r16:
+                if tp is None:
+                    loc, peer = yb, None
+                else:
+                    loc, peer = (None, None) if yb is None else (tp.y[yb].data_ptr(), tp.y_peer[yb].data_ptr())
+                k("rmsnorm", lambda: L.hm_rmsnorm_residual_bf16(self.x.data_ptr(), loc, peer, wt, M, d, cfg.eps,
+                                                                self.h.data_ptr(), mp, st))
+            elif tp is None:   # (hm_rmsnorm_residual2 without a second partial: the d <= 4096 kernel or any-d one)
                 k("rmsnorm", lambda: L.hm_rmsnorm_residual2(self.x.data_ptr(), yb, None, wt, M, d, cfg.eps,
                                                             self.h.data_ptr(), mp, st))
             else:
@@ -413,16 +435,24 @@ class Forward:
                                                   self.cache.n_slots, M, st))
             epi_r = EPI_RESIDUAL if self.residual_in_gemm else EPI_F32
             y_o = self.x.data_ptr() if self.residual_in_gemm else y_out(0)
-            k("gemm_o", lambda: L.hm_gemm(epi_r, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
-                                          M, d, hd_all, None, None, 0, y_o, d, None, None, mp, st))
+            if r16:   # the projection stored in bf16 (EPI_STORE) for the bf16 residual add in the norm
+                k("gemm_o", lambda: L.hm_gemm(EPI_STORE, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
+                                              M, d, hd_all, None, y_o, d, None, 0, None, None, mp, st))
+            else:
+                k("gemm_o", lambda: L.hm_gemm(epi_r, self.attn.data_ptr(), hd_all, layer["wo"].data_ptr(), hd_all,
+                                              M, d, hd_all, None, None, 0, y_o, d, None, None, mp, st))
             allreduce_sync()
             norm(None if self.residual_in_gemm else (y if tp is None else 0), layer["ln2"].data_ptr())
             k("gemm_gate_up", lambda: L.hm_gemm(EPI_SWIGLU, self.h.data_ptr(), d, layer["wgu"].data_ptr(), d, M,
                                                 2 * cfg.ffn, d, None, self.act.data_ptr(), cfg.ffn, None, 0, None,
                                                 None, mp, st))
             y_d = self.x.data_ptr() if self.residual_in_gemm else y_out(1)
-            k("gemm_down", lambda: L.hm_gemm(epi_r, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
-                                             cfg.ffn, M, d, cfg.ffn, None, None, 0, y_d, d, None, None, mp, st))
+            if r16:
+                k("gemm_down", lambda: L.hm_gemm(EPI_STORE, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
+                                                 cfg.ffn, M, d, cfg.ffn, None, y_d, d, None, 0, None, None, mp, st))
+            else:
+                k("gemm_down", lambda: L.hm_gemm(epi_r, self.act.data_ptr(), cfg.ffn, layer["wd"].data_ptr(),
+                                                 cfg.ffn, M, d, cfg.ffn, None, None, 0, y_d, d, None, None, mp, st))
             allreduce_sync()
         norm(None if self.residual_in_gemm else (y if tp is None else 1), w.final_ln.data_ptr())
         if logits_out is not None:

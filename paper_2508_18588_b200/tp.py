@@ -20,7 +20,7 @@ from __future__ import annotations
 class TensorParallel:
     """Symmetric buffers + barrier state of one GPU of a TP pair (process group `group`, two ranks)."""
 
-    def __init__(self, group, max_rows: int, d_model: int, device):
+    def __init__(self, group, max_rows: int, d_model: int, device, dtype=None):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
@@ -30,13 +30,15 @@ class TensorParallel:
         self.rank = dist.get_rank(group)
         self.peer = 1 - self.rank
         self.device = torch.device(device)
+        dtype = dtype or torch.bfloat16            # the forward's residual dtype (bf16 or fp32 partials)
         n = max_rows * d_model
-        # one symmetric allocation: [2 partial buffers of max_rows x d fp32][flag words]
-        self.buf = symm_mem.empty(2 * n + 64, dtype=torch.float32, device=self.device)
+        tail = 256 // torch.tensor([], dtype=dtype).element_size()   # 256 bytes of flag words
+        # one symmetric allocation: [2 partial buffers of max_rows x d][flag words]
+        self.buf = symm_mem.empty(2 * n + tail, dtype=dtype, device=self.device)
         self.buf.zero_()
         name = group.group_name if hasattr(group, "group_name") else dist.group.WORLD.group_name
         self.handle = symm_mem.rendezvous(self.buf, name)
-        peer_buf = self.handle.get_buffer(self.peer, (2 * n + 64,), torch.float32)
+        peer_buf = self.handle.get_buffer(self.peer, (2 * n + tail,), dtype)
         self.y = [self.buf[i * n:(i + 1) * n].view(max_rows, d_model) for i in range(2)]
         self.y_peer = [peer_buf[i * n:(i + 1) * n].view(max_rows, d_model) for i in range(2)]
         flags = self.buf[2 * n:].view(torch.int32)

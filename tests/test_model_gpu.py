@@ -314,9 +314,10 @@ def test_fused_qkv_rope_matches_unfused(torch, cfg_name):
     pos = np.concatenate([np.arange(s, s + n) for s, n in zip(starts, lens)])
     slot = np.concatenate([np.full(n, i) for i, n in enumerate(lens)])
     outs = []
-    for fused, resid in ((True, False), (False, False), (True, True)):
+    for fused, resid, res_dtype in ((True, False, "bf16"), (False, False, "bf16"), (True, False, "fp32"),
+                                    (True, True, "fp32")):
         cache = Mo.KVCache(cfg, 2, 160, "cuda")
-        f = Mo.Forward(w, cache, 64, "cuda")
+        f = Mo.Forward(w, cache, 64, "cuda", residual=res_dtype)
         f.fused_qkv_rope = fused
         f.residual_in_gemm = resid   # residual add in the O / down GEMM epilogues: the same fp32 adds
         logits = torch.empty(T, cfg.vocab, dtype=torch.bfloat16, device="cuda")
@@ -324,9 +325,11 @@ def test_fused_qkv_rope_matches_unfused(torch, cfg_name):
                    max(lens), logits_out=logits)
         torch.cuda.synchronize()
         outs.append((logits.clone(), am.clone(), cache.k(0).clone(), cache.v(cfg.n_layers - 1).clone()))
-    for other in outs[1:]:
-        for a, b in zip(outs[0], other):
-            assert torch.equal(a, b)
+    # bf16 residual: fused == unfused; fp32 residual: add in the norm == add in the GEMM epilogue
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    for a, b in zip(outs[2], outs[3]):
+        assert torch.equal(a, b)
 
 
 def test_tiny_engine_spec_equals_greedy_and_reference_replay(torch):

@@ -43,7 +43,7 @@ def _worker(rank, port, out):
     w = Weights(cfg, dev, seed=5, tp_rank=rank, tp_size=2)
     cache = KVCache(w.cfg, 4, 128, dev)
     fwd = Forward(w, cache, 256, dev)
-    fwd.tp = TensorParallel(dist.group.WORLD, 256, cfg.d_model, dev)
+    fwd.tp = TensorParallel(dist.group.WORLD, 256, cfg.d_model, dev, dtype=fwd.x.dtype)
     g = np.random.default_rng(3)
     P = 50
     toks = torch.as_tensor(g.integers(0, cfg.vocab, size=4 * P).astype(np.int32)).to(dev)
