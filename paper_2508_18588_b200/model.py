@@ -9,7 +9,7 @@ Forward (M rows = all live sequences' verify rows):
   embed -> L x [RMSNorm -> QKV GEMM(+bias) -> RoPE + KV append -> attention
   -> O GEMM (+= residual) -> RMSNorm -> gate/up GEMM with SwiGLU epilogue
   -> down GEMM (+= residual)] -> RMSNorm -> LM head GEMM with argmax epilogue.
-Residual stream fp32; GEMM operands bf16; accumulators fp32 (TMEM).
+Residual stream bf16 (fp32 optional, Forward(residual=...)); GEMM operands bf16; accumulators fp32 (TMEM).
 """
 
 from __future__ import annotations
