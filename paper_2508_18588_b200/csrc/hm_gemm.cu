@@ -370,7 +370,7 @@ k_gemm(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensor
           uint8_t* b = a + C::kABytes;
           mbar_arrive_expect_tx(&full[s], C::kStageBytes);
           tma_load_2d(&tmX, &full[s], a, kb * BK, m_blk * BM);
-          tma_load_2d(&tmW, &full[s], b, kb * BK, n_blk * BN);
+          tma_load_2d(&tmW, &full[s], b, kb * BK, n_blk * BN);   // (evict-first W measured slower)
         }
       }
     }
