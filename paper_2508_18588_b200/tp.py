@@ -6,7 +6,8 @@ an fp32 partial of the full [rows, d] output).  The all-reduce of those partials
 GPU's O / down GEMM writes its partial straight into a symmetric-memory buffer (mapped on both GPUs over
 NVLink), a peer-memory barrier kernel (hm_tp_barrier) orders the two GPUs, and the next RMSNorm reads both
 partials in place -- local from HBM, the peer's over NVLink -- summing y0 + y1 in the same order on both GPUs
-(hm_rmsnorm_residual2), so the replicated residual stream stays bit-identical across the pair.  Two buffers
+(hm_rmsnorm_residual_bf16 with the default bf16 residual stream, hm_rmsnorm_residual2 with fp32), so the
+replicated residual stream stays bit-identical across the pair.  Two buffers
 alternate (O -> buffer 0, down -> buffer 1), so one barrier per all-reduce is enough: a GPU cannot overwrite
 a buffer before its peer has passed the barrier that follows the peer's read of it.
 
