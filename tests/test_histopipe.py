@@ -99,3 +99,18 @@ def test_plan_makespan_balances_groups():
     # the reference's gradient plan gives the short group the workers (its training overlaps the long tail)
     assert W.plan_allocation([1500.0, 6000.0], 4, 0.0, m, precision=0.01).per_group_workers == [3, 1]
     assert not W.plan_makespan([1.0, 2.0, 3.0], 2, m).feasible
+
+
+def test_plan_routes_layout_and_errors():
+    """Host side of device routing: send order (destination, prompt, input order), per-destination counts and
+    token totals, and offsets into the flat send buffer."""
+    import numpy as np
+    plan = W.plan_routes([5, 2, 5, 9, 2], [3, 4, 5, 6, 7], {2: 1, 5: 0, 9: 1}, 2)
+    assert plan.order.tolist() == [0, 2, 1, 4, 3]
+    assert plan.counts.tolist() == [2, 3] and plan.tok_counts.tolist() == [8, 17]
+    assert plan.dst_off.tolist() == [0, 3, 8, 12, 19]
+    empty = W.plan_routes([], [], {}, 3)
+    assert empty.counts.tolist() == [0, 0, 0] and len(empty.order) == 0
+    with pytest.raises(ValueError):
+        W.plan_routes([1], [4], {1: 3}, 2)
+    assert np.array_equal(W.plan_routes([7], [1], {7: 0}, 1).dst_off, [0])
