@@ -111,3 +111,15 @@ def test_c_oracle_derived_digest():
             h.update(json.dumps(tpi).encode())
         assert h.hexdigest() == g["replay_sha"]
         assert stats.sum(axis=0).tolist() == g["stats"]
+
+
+def test_oracle_branch0_is_reference_draft(golden):
+    """oracle.draft_branches (the checker of hs_lookup_branches): branch 0 equals the reference's
+    extract_draft output on the golden corpora, and branch masses are non-increasing."""
+    from oracle import hs_oracle as O
+    for c in golden("drafts.json.gz")[:60]:
+        corpus = [(list(t), float(r)) for t, r in c["corpus"]]
+        for q in c["queries"]:
+            br, ms = O.draft_branches(corpus, q["prefix"], q["window"], 4)
+            assert (br[0] if br else []) == q["tokens"], q
+            assert all(a >= b for a, b in zip(ms, ms[1:]))
